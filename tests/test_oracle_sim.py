@@ -1,0 +1,121 @@
+"""Pins for the oracle's NATTENSim and brute-force tile visits (§3.2).
+
+The paper prints the simulator's results for the HunyuanVideo shape (Fig.4,
+Tab.3) and FLUX 4K (Tab.4); the end-to-end columns follow from the op-level
+bound with the Amdahl relation of §4 (share of SA from Tab.1), so matching all
+printed cells pins the window/stride/tile-range logic.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+
+
+def _e2e(share, steps, sa_steps, op_speedup):
+    gna_frac = (steps - sa_steps) / steps
+    return 1.0 / ((1.0 - share) + share * ((1.0 - gna_frac) + gna_frac / op_speedup))
+
+
+def test_fig4_hunyuan_anchors():
+    g = GOLD["fig4_hunyuan"]
+    na = O.sim(O.Params(g["spatial"], g["window"], (1, 1, 1)), g["tq"], g["tk"])
+    assert round(na["bound"], 1) == g["na_speedup_1dp"]
+    assert not na["perfectly_block_sparse"]
+    cross = O.sim(O.Params(g["spatial"], g["window"], (1, 8, 8)), g["tq"], g["tk"])
+    assert cross["bound"] > g["s188_speedup_min"]
+    bs = O.sim(O.Params(g["spatial"], g["window"], g["blocksparse_stride"]), g["tq"], g["tk"])
+    assert round(bs["bound"], 1) == g["blocksparse_speedup_1dp"]
+    assert bs["perfectly_block_sparse"]
+    # "equivalent to its FLOP-wise speedup"
+    n = int(np.prod(g["spatial"]))
+    assert abs(bs["bound"] - n / np.prod(g["window"])) < 1e-9
+
+
+def test_tab3_hunyuan_91pct_all_cells():
+    g = GOLD["tab3_hunyuan_91"]
+    f = GOLD["fig4_hunyuan"]
+    n = int(np.prod(f["spatial"]))
+    flop = n / np.prod(f["window"])
+    for row in g["rows"]:
+        r = O.sim(O.Params(f["spatial"], f["window"], row["stride"]), f["tq"], f["tk"])
+        got = _e2e(g["sa_share"], g["steps"], row["sa_steps"], r["bound"])
+        # 13 of 14 cells agree to the printed 2 decimals; (1,1,8)/0 SA steps gives
+        # 1.983 vs the printed 1.99 (the share 60.7% is itself rounded) -> 0.008.
+        assert abs(got - row["natten_sim"]) <= 0.008, (row, got)
+        assert abs(_e2e(g["sa_share"], g["steps"], row["sa_steps"], flop) - row["flopwise"]) <= 0.005
+
+
+def test_tab3_mean_based_bound_does_not_reproduce():
+    """Reading R11: the paper's bound is the max over Q tiles ('worst case of all
+    Q tiles'); a mean-based bound misses the printed NA cell."""
+    f = GOLD["fig4_hunyuan"]
+    g = GOLD["tab3_hunyuan_91"]
+    r = O.sim(O.Params(f["spatial"], f["window"], (1, 1, 1)), f["tq"], f["tk"])
+    assert abs(_e2e(g["sa_share"], g["steps"], 0, r["bound_mean"]) - 1.73) > 0.05
+
+
+def test_tab4_flux_all_cells():
+    """Tab.4 with tile shapes T_Q=(16,16), T_KV=(16,8) (the paper does not print
+    the FLUX tiles; this is the reading that reproduces all six cells)."""
+    g = GOLD["tab4_flux_4k"]
+    for row in g["rows"]:
+        r = O.sim(O.Params(g["spatial"], g["window"], row["stride"]), (16, 16), (16, 8))
+        got = _e2e(g["sa_share"], g["steps"], row["sa_steps"], r["bound"])
+        assert abs(got - row["natten_sim"]) <= 0.005 + 1e-9, (row, got)
+    r = O.sim(O.Params(g["spatial"], g["window"], (16, 16)), (16, 16), (16, 8))
+    assert r["perfectly_block_sparse"]
+    assert round(r["bound"], 1) == GOLD["sparsity"]["flux_flopwise_1dp"]
+
+
+def test_sim_self_attention_and_sandwich():
+    """w = extent -> bound 1 (SPEC 'TRIVIAL'); 1 <= bound <= FLOP-wise always."""
+    r = O.sim(O.Params((16, 24), (16, 24), (1, 1)), (4, 8), (4, 8))
+    assert r["bound"] == 1.0
+    rng = np.random.default_rng(3)
+    for _ in range(40):
+        L = [int(x) for x in rng.integers(4, 40, 2)]
+        w = [int(rng.integers(1, l + 1)) for l in L]
+        s = [int(rng.integers(1, x + 1)) for x in w]
+        tq = [int(rng.choice([1, 2, 4, 8])) for _ in L]
+        tk = [int(rng.choice([1, 2, 4, 8])) for _ in L]
+        r = O.sim(O.Params(L, w, s), tq, tk)
+        nk = np.prod([-(-l // t) for l, t in zip(L, tk)])
+        assert 1.0 <= r["bound"] <= nk
+        # tile-level bound never beats FLOP-wise in the absence of padding effects
+        if all(l % t == 0 for l, t in zip(L, tk)):
+            assert r["bound"] <= np.prod(L) / np.prod(w) + 1e-9
+
+
+def test_spec_1d_examples():
+    """SPEC tiler examples: L=8,w=4,s=4,T=4 -> 1 tile each; w=8 -> both tiles."""
+    v = O.visits_bruteforce(O.Params((8,), (4,), (4,)), (4,), (4,))
+    assert (v.sum(1) == 1).all()
+    v = O.visits_bruteforce(O.Params((8,), (8,), (1,)), (4,), (4,))
+    assert (v.sum(1) == 2).all()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_sim_matches_multid_bruteforce(seed):
+    """The per-axis simulator equals the multi-D brute force (enumerating every
+    query's neighbourhood) on random small grids: checks separability."""
+    rng = np.random.default_rng(100 + seed)
+    L = [int(x) for x in rng.integers(3, 18, 3)]
+    w = [int(rng.integers(1, l + 1)) for l in L]
+    s = [int(rng.integers(1, x + 1)) for x in w]
+    causal = [bool(x) for x in rng.integers(0, 2, 3)]
+    tq = [int(rng.choice([1, 2, 4])) for _ in L]
+    tk = [int(rng.choice([1, 2, 4])) for _ in L]
+    p = O.Params(L, w, s, causal=causal)
+    vis = O.visits_bruteforce(p, tq, tk)
+    r = O.sim(p, tq, tk)
+    assert vis.sum(1).max() == r["visited_max"]
+    assert abs(vis.sum(1).mean() - r["visited_mean"]) < 1e-9
+    full = O.full_bruteforce(p, tq, tk, vis)
+    pbs = bool((full[vis.astype(bool)] == 1).all())
+    if all(l % t == 0 for l, t in zip(L, tk)):
+        assert pbs == r["perfectly_block_sparse"]
