@@ -1,0 +1,157 @@
+/*
+ * gna.h -- C ABI of the B200 (sm_100a) Generalized Neighborhood Attention
+ * forward library (libgna_b200.so).  arXiv 2504.16922.
+ *
+ * Citations: "P:<line> §x" = /root/reference/PAPER.md line / section.
+ *
+ * Operation (§3.1, §2.2).  For every batch b, head h and
+ * query token q of a 1-3 axis token grid, GNA attends the neighbourhood
+ * N(q) = K_0(q) x K_1(q) x K_2(q), where per axis (extent L, window w,
+ * stride s, dilation d, causal flag):
+ *   - keys of another dilation class (t mod d) are never attended;
+ *   - queries are grouped by s inside their class; a group shares the window
+ *     of its leader, the center-most member, right-biased;
+ *   - the leader's window has floor(w/2) keys on the left and is
+ *     shifted inward at borders so every query sees w keys;
+ *   - causal axes (cited only) use DESIGN.md reading R4.
+ *   out[q] = softmax_k(scale * q.k) v,   lse[q] = ln sum_k exp(scale * q.k).
+ *
+ * Layout (a build decision -- the paper states none; heads-last as NATTEN):
+ *   q, k, v, out : bf16 [batch][s0][s1][s2][heads][head_dim], contiguous
+ *   lse          : fp32 [batch][s0][s1][s2][heads]
+ *   1-D problems pass spatial = {L, 1, 1}; unused axes must be exactly
+ *   window = stride = dilation = 1, causal = 0.
+ *
+ * Pipeline behind gna_forward (§3.3, re-designed for sm_100a):
+ *   1. token permute (gna_permute): Q, K, V -> tile-contiguous boxes, per
+ *      dilation class, zero-padded;
+ *   2. fused attention (gna_attention_permuted): analytic per-Q-tile KV box
+ *      ranges, TMA + mbarrier pipeline, tcgen05 MMAs with TMEM
+ *      accumulators, online softmax, fine-grained mask only on partial tiles
+ *      (P:627-630); O + LSE epilogue;
+ *   3. inverse permute (gna_unpermute): O, LSE back to the user layout,
+ *      padding cropped.
+ *
+ * Conventions
+ *   - Return codes: GNA_OK, GNA_EINVAL (argument; nothing is launched),
+ *     GNA_EUNSUPPORTED (head_dim/dtype/device), GNA_ECUDA, GNA_ENOMEM.
+ *     gna_last_error() returns a thread-local message naming the argument.
+ *   - All tensor pointers are DEVICE pointers owned by the caller, 16-byte
+ *     aligned; the library never frees them.  Work is enqueued on the given
+ *     stream (NULL = legacy default stream); no host synchronisation except in
+ *     the gna_debug_* exports, which copy small arrays to host memory.
+ *   - Workspace: the permuted Q/K/V/O/LSE buffers and the work list come from
+ *     the caller's workspace (gna_args.workspace, sized by
+ *     gna_workspace_size) or, when NULL, from a per-device grow-only cache
+ *     owned by the library (mutex-guarded), freed by gna_release_workspace().
+ *   - There is no CPU fallback: a missing sm_100 device is GNA_EUNSUPPORTED.
+ *   - Validation: 1 <= stride <= window, window*dilation <=
+ *     extent, all values >= 1, causal in {0,1}, batch, heads >= 1,
+ *     head_dim in {32, 64, 128}.
+ */
+#ifndef GNA_B200_H
+#define GNA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GNA_OK 0
+#define GNA_EINVAL 1
+#define GNA_EUNSUPPORTED 2
+#define GNA_ECUDA 3
+#define GNA_ENOMEM 4
+
+#define GNA_DTYPE_BF16 0
+
+/* flags */
+#define GNA_FLAG_SYNC_CHECK 1 /* synchronize + check after each launch (debug) */
+
+typedef struct gna_args {
+    const void *q, *k, *v; /* device bf16 [B][s0][s1][s2][H][D] */
+    void *out;             /* device bf16, same shape */
+    float *lse;            /* device fp32 [B][s0][s1][s2][H]; may be NULL */
+    int batch, heads, head_dim;
+    int spatial[3], window[3], stride[3], dilation[3], causal[3];
+    float scale;            /* <= 0 -> 1/sqrt(head_dim) */
+    int dtype;              /* GNA_DTYPE_BF16 */
+    void *stream;           /* cudaStream_t */
+    void *workspace;        /* optional caller workspace (device, 256-B aligned) */
+    size_t workspace_bytes;
+    int box[3];             /* permutation box / KV tile override (powers of two,
+                               volume 64 or 128); {0,0,0} = planner's choice */
+    long long work_begin;   /* Q-tile splitting: global work-item range [begin, end) */
+    long long work_end;     /* over (batch*heads) x items; end <= 0 -> all   */
+    int flags;
+} gna_args;
+
+/* Plan summary for a problem (host struct, filled by gna_plan_info). */
+typedef struct gna_plan_info_t {
+    int box[3];             /* KV tile = permutation box */
+    int q_sub[3];           /* 128-row Q sub-tile shape (tokens) */
+    int box_vol;
+    int padded_head_dim;
+    int n_classes;          /* dilation classes */
+    int n_boxes_per_class;  /* padded box grid size */
+    long long n_items;      /* work items per (batch, head) */
+    long long n_work;       /* n_items * batch * heads */
+    long long n_paired;     /* items with two Q sub-tiles */
+    long long kv_stages_total; /* sum over items of 128-row KV stages visited */
+    long long visited_max;  /* max KV boxes visited by one work item */
+    long long dense_boxes;  /* KV boxes per class covering all keys */
+    double bound;           /* NATTENSim bound at these tiles: dense / visited_max */
+    long long kept_pairs;   /* sum_q |N(q)| over one (batch, head) */
+    size_t workspace_bytes;
+} gna_plan_info_t;
+
+/* Full forward: permute -> attention -> inverse permute, on the legacy default
+ * stream with the library workspace.  Arguments as in gna_args. */
+int gna_forward(const void *q, const void *k, const void *v, void *out, float *lse,
+                int batch, int heads, int head_dim, const int spatial[3], const int window[3],
+                const int stride[3], const int dilation[3], const int causal[3], float scale);
+
+/* Full forward with every option of gna_args. */
+int gna_forward_ex(const gna_args *a);
+
+/* Stages, for timing and for hoisting the permutation across layers
+ * (P:609-611).  They share the workspace of `a` (library cache if NULL). */
+int gna_permute(const gna_args *a);            /* q,k,v -> permuted Q,K,V */
+int gna_attention_permuted(const gna_args *a); /* permuted Q,K,V -> permuted O, LSE */
+int gna_unpermute(const gna_args *a);          /* permuted O, LSE -> out, lse */
+
+/* Bytes of caller workspace gna_forward_ex needs for `a`. */
+int gna_workspace_size(const gna_args *a, size_t *bytes);
+
+/* Plan summary (host only, no device work). */
+int gna_plan_info(const gna_args *a, gna_plan_info_t *info);
+
+/* Debug exports (device computation, copied to HOST memory, synchronous).
+ * windows: int32 [s0*s1*s2][3][3] = per token, per axis {class, start, end}
+ *          in class-local indices (keys are c + d*j, j in [start, end)).
+ * visits : int32 [n_classes * n_sub][10] = {class, sub, lo0, hi0, lo1, hi1,
+ *          lo2, hi2, n_full, nonempty}: per 128-row Q sub-tile the KV box range
+ *          per axis and the number of boxes in it that need no mask. */
+int gna_debug_windows(const gna_args *a, int32_t *host_out);
+int gna_debug_visits(const gna_args *a, int32_t *host_out, long long *n_records);
+/* work list: int32 [n_items][4] = {class, subA, subB (-1 = none), kv_boxes} */
+int gna_debug_worklist(const gna_args *a, int32_t *host_out, long long *n_items);
+
+/* Free the library-owned workspace cache of the current device. */
+int gna_release_workspace(void);
+
+/* Thread-local message for the last non-OK return. */
+const char *gna_last_error(void);
+
+/* 1 if the current device is sm_100 and the kernels are loadable. */
+int gna_device_supported(void);
+
+/* Library version string. */
+const char *gna_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNA_B200_H */

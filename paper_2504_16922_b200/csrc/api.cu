@@ -1,0 +1,689 @@
+// api.cu -- host runtime behind the C ABI (include/gna.h): validation, the
+// tile planner, the plan cache, workspace management, TMA descriptor
+// encoding and the three launches of the GNA forward.
+//
+// Planner (§3.2 tile-size design, P:577-582 perfectly block-sparse
+// rule, P:773-778 windows divisible by T_KV):
+//   * dilation is folded into C = d0*d1*d2 classes, each an independent
+//     non-dilated sub-grid (reading R6) with its own box grid;
+//   * the permutation box is the KV tile: power-of-two extents per axis,
+//     volume 64 or 128 tokens; a Q sub-tile is 128 rows (1 or 2 boxes);
+//   * Q sub-tiles with identical analytic KV ranges are paired into one CTA
+//     (2 x 128 rows share every K/V stage); leftovers are paired with their
+//     neighbour only if the union range costs less than running alone;
+//   * the box minimising the modelled tensor work is chosen.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <array>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/gna.h"
+#include "geom.cuh"
+#include "kernels.h"
+
+namespace gna {
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define GNA_CUDA_TRY(expr)                                                                         \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            return fail(e_ == cudaErrorMemoryAllocation ? GNA_ENOMEM : GNA_ECUDA,                  \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                       \
+        }                                                                                          \
+    } while (0)
+
+int ilog2(int x) {
+    int l = 0;
+    while ((1 << l) < x) ++l;
+    return l;
+}
+int pow2ceil(int x) { return 1 << ilog2(x < 1 ? 1 : x); }
+
+// --------------------------------------------------------------- validation
+int validate(const gna_args* a, bool need_ptrs) {
+    if (!a) return fail(GNA_EINVAL, "args is NULL");
+    if (a->dtype != GNA_DTYPE_BF16) return fail(GNA_EUNSUPPORTED, "dtype: only GNA_DTYPE_BF16 is supported");
+    if (a->batch < 1) return fail(GNA_EINVAL, "batch must be >= 1");
+    if (a->heads < 1) return fail(GNA_EINVAL, "heads must be >= 1");
+    if (a->head_dim != 32 && a->head_dim != 64 && a->head_dim != 128)
+        return fail(GNA_EUNSUPPORTED, "head_dim must be 32, 64 or 128");
+    for (int ax = 0; ax < 3; ++ax) {
+        char buf[256];
+        const int L = a->spatial[ax], w = a->window[ax], s = a->stride[ax], d = a->dilation[ax], c = a->causal[ax];
+        if (L < 1 || w < 1 || s < 1 || d < 1) {
+            snprintf(buf, sizeof buf, "axis %d: spatial/window/stride/dilation must be >= 1", ax);
+            return fail(GNA_EINVAL, buf);
+        }
+        if (c != 0 && c != 1) {
+            snprintf(buf, sizeof buf, "axis %d: causal must be 0 or 1", ax);
+            return fail(GNA_EINVAL, buf);
+        }
+        if (s > w) {
+            snprintf(buf, sizeof buf, "axis %d: stride %d > window %d leaves holes (P:428-430)", ax, s, w);
+            return fail(GNA_EINVAL, buf);
+        }
+        if (static_cast<long long>(w) * d > L) {
+            snprintf(buf, sizeof buf, "axis %d: window*dilation %lld exceeds extent %d", ax,
+                     static_cast<long long>(w) * d, L);
+            return fail(GNA_EINVAL, buf);
+        }
+        if (L == 1 && (w != 1 || s != 1 || d != 1 || c != 0)) {
+            snprintf(buf, sizeof buf, "axis %d: unused axis must have window=stride=dilation=1, causal=0", ax);
+            return fail(GNA_EINVAL, buf);
+        }
+        const int B = a->box[ax];
+        if (B != 0 && (B < 1 || B > 128 || (B & (B - 1)) != 0)) {
+            snprintf(buf, sizeof buf, "axis %d: box override must be a power of two <= 128", ax);
+            return fail(GNA_EINVAL, buf);
+        }
+    }
+    const int bo = a->box[0] * a->box[1] * a->box[2];
+    if ((a->box[0] | a->box[1] | a->box[2]) != 0 && bo != 64 && bo != 128)
+        return fail(GNA_EINVAL, "box override volume must be 64 or 128");
+    const long long N = static_cast<long long>(a->spatial[0]) * a->spatial[1] * a->spatial[2];
+    if (N * a->heads * a->batch > (1LL << 40)) return fail(GNA_EINVAL, "problem too large");
+    if (need_ptrs) {
+        const void* ptrs[4] = {a->q, a->k, a->v, a->out};
+        const char* names[4] = {"q", "k", "v", "out"};
+        for (int i = 0; i < 4; ++i) {
+            if (!ptrs[i]) return fail(GNA_EINVAL, std::string(names[i]) + " is NULL");
+            if (reinterpret_cast<uintptr_t>(ptrs[i]) % 16) return fail(GNA_EINVAL, std::string(names[i]) + " not 16-byte aligned");
+        }
+        if (a->lse && reinterpret_cast<uintptr_t>(a->lse) % 4) return fail(GNA_EINVAL, "lse not 4-byte aligned");
+    }
+    return GNA_OK;
+}
+
+// ------------------------------------------------------------------- plans
+struct Plan {
+    Geometry g;  // batch/heads filled per call
+    std::vector<int4> items;
+    gna_plan_info_t info;
+    std::map<int, int4*> dev_items;  // per device copy of the work list
+    std::mutex mu;
+};
+
+Geometry make_geometry(const gna_args* a, const int B[3], const int QB[3]) {
+    Geometry g{};
+    for (int ax = 0; ax < 3; ++ax) {
+        g.ax[ax] = Axis{a->spatial[ax], a->window[ax], a->stride[ax], a->dilation[ax], a->causal[ax]};
+        g.B[ax] = B[ax];
+        g.logB[ax] = ilog2(B[ax]);
+        g.QB[ax] = QB[ax];
+        const int Lmax = ceil_div(a->spatial[ax], a->dilation[ax]);
+        const int ext = QB[ax] * B[ax];
+        g.nq[ax] = ceil_div(Lmax, ext);
+        g.nb[ax] = g.nq[ax] * QB[ax];
+    }
+    g.box_vol = B[0] * B[1] * B[2];
+    g.nbox = g.nb[0] * g.nb[1] * g.nb[2];
+    g.nsub = g.nq[0] * g.nq[1] * g.nq[2];
+    g.ncls = a->dilation[0] * a->dilation[1] * a->dilation[2];
+    g.D = a->head_dim;
+    g.Dp = a->head_dim < 64 ? 64 : a->head_dim;
+    g.heads = a->heads;
+    g.batch = a->batch;
+    return g;
+}
+
+struct Built {
+    std::vector<int4> items;
+    double cost = 0;
+    long long stages = 0, paired = 0, vmax = 0;
+};
+
+constexpr double kSingleCost = 1.3;  // relative cost of a 128-row CTA stage vs a paired one (2.0)
+
+Built build_items(const Geometry& g) {
+    Built out;
+    const int kpb = 128 / g.box_vol;
+    auto stages_of = [&](const int lo[3], const int hi[3]) {
+        const long long n = static_cast<long long>(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
+        return (n + kpb - 1) / kpb;
+    };
+    for (int cls = 0; cls < g.ncls; ++cls) {
+        std::map<std::array<int, 6>, std::vector<int>> groups;
+        std::vector<std::array<int, 6>> rng(g.nsub);
+        for (int sub = 0; sub < g.nsub; ++sub) {
+            int lo[3], hi[3];
+            if (!sub_range(g, cls, sub, lo, hi)) continue;
+            std::array<int, 6> key{lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]};
+            rng[sub] = key;
+            groups[key].push_back(sub);
+        }
+        std::vector<int> left;
+        for (auto& kv : groups) {
+            const auto& v = kv.second;
+            size_t i = 0;
+            for (; i + 1 < v.size(); i += 2) out.items.push_back(make_int4(cls, v[i], v[i + 1], 0));
+            if (i < v.size()) left.push_back(v[i]);
+        }
+        std::sort(left.begin(), left.end());
+        for (size_t i = 0; i < left.size();) {
+            const auto& ra = rng[left[i]];
+            const int la[3] = {ra[0], ra[2], ra[4]}, ha[3] = {ra[1], ra[3], ra[5]};
+            if (i + 1 < left.size()) {
+                const auto& rb = rng[left[i + 1]];
+                const int lb[3] = {rb[0], rb[2], rb[4]}, hb[3] = {rb[1], rb[3], rb[5]};
+                int lu[3], hu[3];
+                for (int a = 0; a < 3; ++a) {
+                    lu[a] = std::min(la[a], lb[a]);
+                    hu[a] = std::max(ha[a], hb[a]);
+                }
+                const double pair_cost = 2.0 * stages_of(lu, hu);
+                const double solo_cost = kSingleCost * (stages_of(la, ha) + stages_of(lb, hb));
+                if (pair_cost <= solo_cost) {
+                    out.items.push_back(make_int4(cls, left[i], left[i + 1], 0));
+                    i += 2;
+                    continue;
+                }
+            }
+            out.items.push_back(make_int4(cls, left[i], -1, 0));
+            i += 1;
+        }
+    }
+    for (auto& it : out.items) {
+        int lo[3], hi[3];
+        sub_range(g, it.x, it.y, lo, hi);
+        if (it.z >= 0) {
+            int lb[3], hb[3];
+            sub_range(g, it.x, it.z, lb, hb);
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::min(lo[a], lb[a]);
+                hi[a] = std::max(hi[a], hb[a]);
+            }
+        }
+        const long long nbx = static_cast<long long>(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
+        it.w = static_cast<int>(nbx);
+        const long long st = (nbx + kpb - 1) / kpb;
+        out.stages += st;
+        out.vmax = std::max(out.vmax, nbx);
+        if (it.z >= 0) ++out.paired;
+        out.cost += (it.z >= 0 ? 2.0 : kSingleCost) * st;
+    }
+    // longest first (approximate LPT under the hardware block scheduler)
+    std::stable_sort(out.items.begin(), out.items.end(), [](const int4& x, const int4& y) {
+        const long long cx = static_cast<long long>(x.w) * (x.z >= 0 ? 2 : 1);
+        const long long cy = static_cast<long long>(y.w) * (y.z >= 0 ? 2 : 1);
+        return cx > cy;
+    });
+    return out;
+}
+
+std::mutex g_plan_mu;
+std::map<std::vector<int>, std::shared_ptr<Plan>> g_plans;
+
+std::vector<int> plan_key(const gna_args* a) {
+    std::vector<int> k;
+    for (int ax = 0; ax < 3; ++ax) {
+        k.push_back(a->spatial[ax]);
+        k.push_back(a->window[ax]);
+        k.push_back(a->stride[ax]);
+        k.push_back(a->dilation[ax]);
+        k.push_back(a->causal[ax]);
+        k.push_back(a->box[ax]);
+    }
+    k.push_back(a->head_dim);
+    return k;
+}
+
+std::shared_ptr<Plan> get_plan(const gna_args* a) {
+    const auto key = plan_key(a);
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it != g_plans.end()) return it->second;
+    }
+    // ---- candidate boxes
+    int cap[3];
+    for (int ax = 0; ax < 3; ++ax) cap[ax] = std::min(128, pow2ceil(ceil_div(a->spatial[ax], a->dilation[ax])));
+    while (cap[0] * cap[1] * cap[2] < 64) {
+        int best = 0;
+        for (int ax = 1; ax < 3; ++ax)
+            if (a->spatial[ax] > a->spatial[best]) best = ax;
+        cap[best] *= 2;
+    }
+    std::vector<std::pair<std::array<int, 3>, std::array<int, 3>>> cands;
+    if (a->box[0] | a->box[1] | a->box[2]) {
+        const int vol = a->box[0] * a->box[1] * a->box[2];
+        if (vol == 128) cands.push_back({{a->box[0], a->box[1], a->box[2]}, {1, 1, 1}});
+        else
+            for (int ax = 0; ax < 3; ++ax) {
+                std::array<int, 3> qb{1, 1, 1};
+                qb[ax] = 2;
+                cands.push_back({{a->box[0], a->box[1], a->box[2]}, qb});
+            }
+    } else {
+        for (int b0 = 1; b0 <= cap[0]; b0 *= 2)
+            for (int b1 = 1; b1 <= cap[1]; b1 *= 2)
+                for (int vol : {128, 64}) {
+                    if (vol % (b0 * b1)) continue;
+                    const int b2 = vol / (b0 * b1);
+                    if (b2 > cap[2]) continue;
+                    if (vol == 128) cands.push_back({{b0, b1, b2}, {1, 1, 1}});
+                    else
+                        for (int ax = 0; ax < 3; ++ax) {
+                            std::array<int, 3> qb{1, 1, 1};
+                            qb[ax] = 2;
+                            cands.push_back({{b0, b1, b2}, qb});
+                        }
+                }
+    }
+    auto plan = std::make_shared<Plan>();
+    double best_cost = 1e300;
+    long long best_pad = 0;
+    for (auto& c : cands) {
+        Geometry g = make_geometry(a, c.first.data(), c.second.data());
+        Built b = build_items(g);
+        const long long pad = static_cast<long long>(g.nbox) * g.box_vol;
+        const bool better = b.cost < best_cost * (1 - 1e-9) ||
+                            (b.cost <= best_cost * (1 + 1e-9) && pad < best_pad);
+        if (better) {
+            best_cost = b.cost;
+            best_pad = pad;
+            plan->g = g;
+            plan->items = std::move(b.items);
+            gna_plan_info_t& in = plan->info;
+            memset(&in, 0, sizeof in);
+            for (int ax = 0; ax < 3; ++ax) {
+                in.box[ax] = g.B[ax];
+                in.q_sub[ax] = g.B[ax] * g.QB[ax];
+            }
+            in.box_vol = g.box_vol;
+            in.padded_head_dim = g.Dp;
+            in.n_classes = g.ncls;
+            in.n_boxes_per_class = g.nbox;
+            in.n_items = static_cast<long long>(plan->items.size());
+            in.n_paired = b.paired;
+            in.kv_stages_total = b.stages;
+            in.visited_max = b.vmax;
+            long long dense = 1;
+            for (int ax = 0; ax < 3; ++ax) dense *= ceil_div(ceil_div(a->spatial[ax], a->dilation[ax]), g.B[ax]);
+            in.dense_boxes = dense;
+            in.bound = b.vmax > 0 ? static_cast<double>(dense) / static_cast<double>(b.vmax) : 0.0;
+        }
+    }
+    // kept pairs per (batch, head): product over axes of the summed window sizes
+    long long kept = 1;
+    for (int ax = 0; ax < 3; ++ax) {
+        const Axis& A = plan->g.ax[ax];
+        long long sum = 0;
+        for (int t = 0; t < A.L; ++t) {
+            const int c = t % A.d;
+            int st, en;
+            window(A, class_extent(A, c), t / A.d, &st, &en);
+            sum += en - st;
+        }
+        kept *= sum;
+    }
+    plan->info.kept_pairs = kept;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) return it->second;
+    g_plans[key] = plan;
+    return plan;
+}
+
+// per-device copy of the work list
+int plan_device_items(Plan& p, int4** out) {
+    int dev = 0;
+    GNA_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(p.mu);
+    auto it = p.dev_items.find(dev);
+    if (it != p.dev_items.end()) {
+        *out = it->second;
+        return GNA_OK;
+    }
+    int4* d = nullptr;
+    const size_t bytes = std::max<size_t>(1, p.items.size()) * sizeof(int4);
+    GNA_CUDA_TRY(cudaMalloc(&d, bytes));
+    if (!p.items.empty()) GNA_CUDA_TRY(cudaMemcpy(d, p.items.data(), p.items.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    p.dev_items[dev] = d;
+    *out = d;
+    return GNA_OK;
+}
+
+// --------------------------------------------------------------- workspace
+struct WsLayout {
+    size_t q, k, v, o, lse, total;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+WsLayout ws_layout(const Geometry& g) {
+    const size_t rows = static_cast<size_t>(perm_rows(g));
+    const size_t tbytes = align256(rows * g.Dp * 2);
+    WsLayout L;
+    L.q = 0;
+    L.k = L.q + tbytes;
+    L.v = L.k + tbytes;
+    L.o = L.v + tbytes;
+    L.lse = L.o + tbytes;
+    L.total = L.lse + align256(rows * 4);
+    return L;
+}
+
+struct DevWs {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+std::mutex g_ws_mu;
+std::map<int, DevWs> g_ws;
+
+int get_workspace(const gna_args* a, size_t need, uint8_t** base) {
+    if (a->workspace) {
+        if (a->workspace_bytes < need) return fail(GNA_EINVAL, "workspace_bytes too small (see gna_workspace_size)");
+        if (reinterpret_cast<uintptr_t>(a->workspace) % 256) return fail(GNA_EINVAL, "workspace not 256-byte aligned");
+        *base = static_cast<uint8_t*>(a->workspace);
+        return GNA_OK;
+    }
+    int dev = 0;
+    GNA_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    DevWs& w = g_ws[dev];
+    if (w.bytes < need) {
+        if (w.ptr) {
+            // a buffer still in use by queued work must not be freed early
+            GNA_CUDA_TRY(cudaDeviceSynchronize());
+            GNA_CUDA_TRY(cudaFree(w.ptr));
+            w.ptr = nullptr;
+            w.bytes = 0;
+        }
+        GNA_CUDA_TRY(cudaMalloc(&w.ptr, need));
+        w.bytes = need;
+    }
+    *base = static_cast<uint8_t*>(w.ptr);
+    return GNA_OK;
+}
+
+// ---------------------------------------------------------------- TMA maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+int make_tmap(CUtensorMap* m, const void* base, const Geometry& g) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const long long rows = perm_rows(g);
+    if (rows >= (1LL << 31)) return fail(GNA_EINVAL, "permuted tensor exceeds 2^31 rows");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.Dp), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Dp) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(g.box_vol)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return GNA_OK;
+}
+
+int check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(GNA_EUNSUPPORTED, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    int maj = 0, min = 0;
+    cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, dev);
+    if (maj != 10 || min != 0) return fail(GNA_EUNSUPPORTED, "device is not sm_100 (B200)");
+    return GNA_OK;
+}
+
+int post_launch(const gna_args* a, cudaStream_t st, const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(GNA_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    if (a->flags & GNA_FLAG_SYNC_CHECK) {
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail(GNA_ECUDA, std::string(what) + " (sync): " + cudaGetErrorString(e));
+    }
+    return GNA_OK;
+}
+
+struct Ctx {
+    std::shared_ptr<Plan> plan;
+    Geometry g;
+    WsLayout L;
+    uint8_t* ws = nullptr;
+    cudaStream_t st = nullptr;
+};
+
+int prepare(const gna_args* a, bool need_ptrs, Ctx* c) {
+    int rc = validate(a, need_ptrs);
+    if (rc) return rc;
+    if ((rc = check_device())) return rc;
+    c->plan = get_plan(a);
+    c->g = c->plan->g;
+    c->g.batch = a->batch;
+    c->g.heads = a->heads;
+    c->L = ws_layout(c->g);
+    c->st = static_cast<cudaStream_t>(a->stream);
+    return get_workspace(a, c->L.total, &c->ws);
+}
+
+int do_permute(const gna_args* a, Ctx& c) {
+    GNA_CUDA_TRY(launch_permute_qkv(c.g, a->q, a->k, a->v, c.ws + c.L.q, c.ws + c.L.k, c.ws + c.L.v, c.st));
+    return post_launch(a, c.st, "permute_qkv");
+}
+
+int do_attention(const gna_args* a, Ctx& c) {
+    int rc;
+    int4* items = nullptr;
+    if ((rc = plan_device_items(*c.plan, &items))) return rc;
+    CUtensorMap tq, tk, tv;
+    if ((rc = make_tmap(&tq, c.ws + c.L.q, c.g))) return rc;
+    if ((rc = make_tmap(&tk, c.ws + c.L.k, c.g))) return rc;
+    if ((rc = make_tmap(&tv, c.ws + c.L.v, c.g))) return rc;
+    AttnParams p{};
+    p.g = c.g;
+    p.items = items;
+    p.n_items = static_cast<long long>(c.plan->items.size());
+    const long long total = p.n_items * a->batch * a->heads;
+    long long wb = a->work_begin, we = a->work_end;
+    if (we <= 0 || we > total) we = total;
+    if (wb < 0) wb = 0;
+    if (wb > we) return fail(GNA_EINVAL, "work_begin > work_end");
+    p.work_begin = wb;
+    p.o_perm = c.ws + c.L.o;
+    p.lse_perm = reinterpret_cast<float*>(c.ws + c.L.lse);
+    const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));
+    p.scale_log2 = scale * 1.4426950408889634f;
+    GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, we - wb, c.st));
+    return post_launch(a, c.st, "gna_attn_sm100");
+}
+
+int do_unpermute(const gna_args* a, Ctx& c) {
+    GNA_CUDA_TRY(launch_unpermute(c.g, c.ws + c.L.o, reinterpret_cast<const float*>(c.ws + c.L.lse), a->out, a->lse,
+                                  c.st));
+    return post_launch(a, c.st, "unpermute");
+}
+
+}  // namespace
+}  // namespace gna
+
+using namespace gna;
+
+extern "C" {
+
+int gna_forward_ex(const gna_args* a) {
+    Ctx c;
+    int rc = prepare(a, true, &c);
+    if (rc) return rc;
+    if ((rc = do_permute(a, c))) return rc;
+    if ((rc = do_attention(a, c))) return rc;
+    return do_unpermute(a, c);
+}
+
+int gna_forward(const void* q, const void* k, const void* v, void* out, float* lse, int batch, int heads,
+                int head_dim, const int spatial[3], const int window[3], const int stride[3], const int dilation[3],
+                const int causal[3], float scale) {
+    if (!spatial || !window || !stride || !dilation || !causal) return fail(GNA_EINVAL, "NULL parameter array");
+    gna_args a;
+    memset(&a, 0, sizeof a);
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.out = out;
+    a.lse = lse;
+    a.batch = batch;
+    a.heads = heads;
+    a.head_dim = head_dim;
+    for (int i = 0; i < 3; ++i) {
+        a.spatial[i] = spatial[i];
+        a.window[i] = window[i];
+        a.stride[i] = stride[i];
+        a.dilation[i] = dilation[i];
+        a.causal[i] = causal[i];
+    }
+    a.scale = scale;
+    a.dtype = GNA_DTYPE_BF16;
+    return gna_forward_ex(&a);
+}
+
+int gna_permute(const gna_args* a) {
+    if (!a || !a->q || !a->k || !a->v) return fail(GNA_EINVAL, "q/k/v NULL");
+    Ctx c;
+    int rc = prepare(a, false, &c);
+    if (rc) return rc;
+    return do_permute(a, c);
+}
+
+int gna_attention_permuted(const gna_args* a) {
+    Ctx c;
+    int rc = prepare(a, false, &c);
+    if (rc) return rc;
+    return do_attention(a, c);
+}
+
+int gna_unpermute(const gna_args* a) {
+    if (!a || !a->out) return fail(GNA_EINVAL, "out NULL");
+    Ctx c;
+    int rc = prepare(a, false, &c);
+    if (rc) return rc;
+    return do_unpermute(a, c);
+}
+
+int gna_workspace_size(const gna_args* a, size_t* bytes) {
+    int rc = validate(a, false);
+    if (rc) return rc;
+    if (!bytes) return fail(GNA_EINVAL, "bytes is NULL");
+    auto plan = get_plan(a);
+    Geometry g = plan->g;
+    g.batch = a->batch;
+    g.heads = a->heads;
+    *bytes = ws_layout(g).total;
+    return GNA_OK;
+}
+
+int gna_plan_info(const gna_args* a, gna_plan_info_t* info) {
+    int rc = validate(a, false);
+    if (rc) return rc;
+    if (!info) return fail(GNA_EINVAL, "info is NULL");
+    auto plan = get_plan(a);
+    *info = plan->info;
+    info->n_work = info->n_items * a->batch * a->heads;
+    Geometry g = plan->g;
+    g.batch = a->batch;
+    g.heads = a->heads;
+    info->workspace_bytes = ws_layout(g).total;
+    return GNA_OK;
+}
+
+int gna_debug_windows(const gna_args* a, int32_t* host_out) {
+    int rc = validate(a, false);
+    if (rc) return rc;
+    if ((rc = check_device())) return rc;
+    if (!host_out) return fail(GNA_EINVAL, "host_out is NULL");
+    auto plan = get_plan(a);
+    const long long N = static_cast<long long>(a->spatial[0]) * a->spatial[1] * a->spatial[2];
+    int32_t* d = nullptr;
+    GNA_CUDA_TRY(cudaMalloc(&d, N * 9 * sizeof(int32_t)));
+    cudaError_t e = launch_debug_windows(plan->g, d, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(host_out, d, N * 9 * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(GNA_ECUDA, std::string("debug_windows: ") + cudaGetErrorString(e));
+    return GNA_OK;
+}
+
+int gna_debug_visits(const gna_args* a, int32_t* host_out, long long* n_records) {
+    int rc = validate(a, false);
+    if (rc) return rc;
+    auto plan = get_plan(a);
+    const long long n = static_cast<long long>(plan->g.ncls) * plan->g.nsub;
+    if (n_records) *n_records = n;
+    if (!host_out) return GNA_OK;  // size query
+    if ((rc = check_device())) return rc;
+    int32_t* d = nullptr;
+    GNA_CUDA_TRY(cudaMalloc(&d, n * 10 * sizeof(int32_t)));
+    cudaError_t e = launch_debug_visits(plan->g, d, 0);
+    if (e == cudaSuccess) e = cudaMemcpy(host_out, d, n * 10 * sizeof(int32_t), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(GNA_ECUDA, std::string("debug_visits: ") + cudaGetErrorString(e));
+    return GNA_OK;
+}
+
+int gna_debug_worklist(const gna_args* a, int32_t* host_out, long long* n_items) {
+    int rc = validate(a, false);
+    if (rc) return rc;
+    auto plan = get_plan(a);
+    if (n_items) *n_items = static_cast<long long>(plan->items.size());
+    if (host_out)
+        for (size_t i = 0; i < plan->items.size(); ++i) {
+            host_out[4 * i + 0] = plan->items[i].x;
+            host_out[4 * i + 1] = plan->items[i].y;
+            host_out[4 * i + 2] = plan->items[i].z;
+            host_out[4 * i + 3] = plan->items[i].w;
+        }
+    return GNA_OK;
+}
+
+int gna_release_workspace(void) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return GNA_OK;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_ws.find(dev);
+    if (it != g_ws.end() && it->second.ptr) {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e == cudaSuccess) e = cudaFree(it->second.ptr);
+        it->second = DevWs{};
+        if (e != cudaSuccess) return fail(GNA_ECUDA, cudaGetErrorString(e));
+    }
+    return GNA_OK;
+}
+
+const char* gna_last_error(void) { return g_last_error.c_str(); }
+
+int gna_device_supported(void) { return check_device() == GNA_OK ? 1 : 0; }
+
+const char* gna_version(void) { return "gna-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,459 @@
+// attn_sm100.cu -- fused GNA attention mainloop for B200 (sm_100a).
+//
+// One CTA = one work item = up to two 128-row Q sub-tiles (A, B) of one
+// (batch, head, dilation class).  The CTA walks the KV boxes of the union of
+// the sub-tiles' analytic ranges (geom.cuh; §3.3): no mask tensor
+// ever exists in HBM, and boxes outside the range are never loaded.
+//
+// Warp roles (320 threads):
+//   warps 0-3  softmax WG0 : rows of sub-tile A, TMEM lanes 0-127, S0/P0, O0
+//   warps 4-7  softmax WG1 : rows of sub-tile B, S1/P1, O1
+//   warp  8    TMA producer: Q sub-tiles once, then K_j, V_j into a smem ring
+//   warp  9    MMA issuer  : tcgen05.mma, one elected lane
+// TMEM (512 columns x 128 lanes, fp32):  S0 [0,128)  S1 [128,256)
+//   O0 [256, 256+Dp)  O1 [384, 384+Dp); P_i (bf16x2) aliases S_i's first 64.
+//
+// Per KV stage j (128 keys), the MMA issue order is
+//   PV0(j-1) -> S0(j) ; PV1(j-1) -> S1(j)
+// so the tensor pipe works on one sub-tile while the softmax warps of the
+// other run, the FA-style ping-pong (P:586-598 describe the CUTLASS Blackwell
+// FMHA the paper builds on; this is an independent sm_100a design).
+//
+// Softmax (online): S is read from TMEM; the fine-grained GNA mask
+// is applied only when some row of the warp does not cover every
+// key of the stage (per-warp generalisation of the paper's perfectly
+// block-sparse predicate, future work P:1054-1058).  The running
+// max used for exp2 is only raised when the row max grows by > 8 (log2
+// units), so O in TMEM is rescaled rarely (threshold trick; values of P stay
+// <= 2^8, exact in bf16 range).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "geom.cuh"
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace gna {
+
+namespace {
+
+template <int DP, int BV>
+struct Cfg {
+    static constexpr int NH = DP / 64;               // 128-byte column chunks ("halves")
+    static constexpr int CHUNK_BYTES = 128 * 128;    // 128 rows x 128 B, one SW128 chunk
+    static constexpr int TILE_BYTES = NH * CHUNK_BYTES;  // 128 rows x DP bf16
+    static constexpr int NS = DP == 128 ? 4 : 8;     // KV ring slots (K and V share it)
+    static constexpr int KPB = 128 / BV;             // boxes per 128-row tile
+    static constexpr int Q_OFF = 0;
+    static constexpr int KV_OFF = 2 * TILE_BYTES;
+    static constexpr int BAR_OFF = KV_OFF + NS * TILE_BYTES;
+    static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
+    static constexpr int THREADS = 320;
+};
+
+struct StageBoxes {
+    int k[2][3];   // box coordinates (class-local box units) of the stage's boxes
+    int dead[2];   // 1 = filler box (odd count), masked entirely
+    int lin[2];    // linear box index inside the class box grid
+};
+
+__device__ __forceinline__ void decode_stage(const Geometry& g, const int lo[3], const int ext[3], int nkv,
+                                             int j, int kpb, StageBoxes& sb) {
+    for (int u = 0; u < kpb; ++u) {
+        int jb = j * kpb + u;
+        sb.dead[u] = jb >= nkv;
+        if (jb >= nkv) jb = 0;
+        const int k2 = jb % ext[2];
+        const int k1 = (jb / ext[2]) % ext[1];
+        const int k0 = jb / (ext[2] * ext[1]);
+        sb.k[u][0] = lo[0] + k0;
+        sb.k[u][1] = lo[1] + k1;
+        sb.k[u][2] = lo[2] + k2;
+        sb.lin[u] = ((lo[0] + k0) * g.nb[1] + (lo[1] + k1)) * g.nb[2] + (lo[2] + k2);
+    }
+}
+
+}  // namespace
+
+template <int DP, int BV>
+__global__ void __launch_bounds__(320, 1)
+    gna_attn_sm100(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tmap_q,
+                   const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v) {
+    using C = Cfg<DP, BV>;
+    constexpr int KPB = C::KPB;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* sgen = smem_raw + (sbase - ptx::smem_u32(smem_raw));
+
+    const Geometry& g = p.g;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    // ---------------------------------------------------------- work item
+    const long long w = static_cast<long long>(blockIdx.x) + p.work_begin;
+    const long long bh = w / p.n_items;
+    const int4 item = p.items[w % p.n_items];
+    const int cls = item.x, subA = item.y, subB = item.z;
+    const bool hasB = subB >= 0;
+
+    int lo[3], hi[3];
+    sub_range(g, cls, subA, lo, hi);
+    if (hasB) {
+        int lb[3], hb[3];
+        sub_range(g, cls, subB, lb, hb);
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = min(lo[a], lb[a]);
+            hi[a] = max(hi[a], hb[a]);
+        }
+    }
+    int ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = hi[a] - lo[a];
+    const int nkv = ext[0] * ext[1] * ext[2];
+    const int nst = (nkv + KPB - 1) / KPB;
+    if (nst <= 0) return;  // uniform for the CTA: empty item
+
+    // rows of this (bh, class) start here in the permuted buffers
+    const long long cls_row0 = ((bh * g.ncls + cls) * static_cast<long long>(g.nbox)) * BV;
+
+    // ---------------------------------------------------------- smem carve
+    const uint32_t sQ = sbase + C::Q_OFF;
+    const uint32_t sKV = sbase + C::KV_OFF;
+    const uint32_t bar0 = sbase + C::BAR_OFF;
+    const uint32_t bar_q = bar0;
+    auto bar_kv_full = [&](int s) { return bar0 + 8u * (1 + s); };
+    auto bar_kv_empty = [&](int s) { return bar0 + 8u * (1 + C::NS + s); };
+    const uint32_t bar_s_full0 = bar0 + 8u * (1 + 2 * C::NS);
+    const uint32_t bar_p_full0 = bar_s_full0 + 16;
+    const uint32_t bar_o_full = bar_p_full0 + 16;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 8 * (1 + 2 * C::NS) + 40);
+
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(bar_q, 1);
+        for (int s = 0; s < C::NS; ++s) {
+            ptx::mbar_init(bar_kv_full(s), 1);
+            ptx::mbar_init(bar_kv_empty(s), 1);
+        }
+        ptx::mbar_init(bar_s_full0, 1);
+        ptx::mbar_init(bar_s_full0 + 8, 1);
+        ptx::mbar_init(bar_p_full0, 128);
+        ptx::mbar_init(bar_p_full0 + 8, 128);
+        ptx::mbar_init(bar_o_full, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 8) {
+        ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == 8) {
+        // ===================================================== TMA producer
+        if (lane == 0) {
+            ptx::tma_prefetch_desc(&tmap_q);
+            ptx::tma_prefetch_desc(&tmap_k);
+            ptx::tma_prefetch_desc(&tmap_v);
+            ptx::mbar_expect_tx(bar_q, (hasB ? 2 : 1) * C::TILE_BYTES);
+            for (int i = 0; i < (hasB ? 2 : 1); ++i) {
+                const int sub = i == 0 ? subA : subB;
+                int sc[3];
+                sub_coords(g, sub, sc);
+                for (int u = 0; u < KPB; ++u) {
+                    // box u of the sub-tile, row-major over the sub-tile's QB box block
+                    const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
+                    const int blin = ((sc[0] * g.QB[0] + u0) * g.nb[1] + (sc[1] * g.QB[1] + u1)) * g.nb[2] +
+                                     (sc[2] * g.QB[2] + u2);
+                    const int row = static_cast<int>(cls_row0 + static_cast<long long>(blin) * BV);
+                    for (int h = 0; h < C::NH; ++h)
+                        ptx::tma_load_2d(sQ + i * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, &tmap_q,
+                                         bar_q, h * 64, row);
+                }
+            }
+            int it = 0;
+            StageBoxes sb;
+            for (int j = 0; j < nst; ++j) {
+                decode_stage(g, lo, ext, nkv, j, KPB, sb);
+                for (int kind = 0; kind < 2; ++kind, ++it) {
+                    const int slot = it % C::NS;
+                    ptx::mbar_wait(bar_kv_empty(slot), ((it / C::NS) & 1) ^ 1);
+                    ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE_BYTES);
+                    const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
+                    for (int u = 0; u < KPB; ++u) {
+                        const int row = static_cast<int>(cls_row0 + static_cast<long long>(sb.lin[u]) * BV);
+                        for (int h = 0; h < C::NH; ++h)
+                            ptx::tma_load_2d(sKV + slot * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, tm,
+                                             bar_kv_full(slot), h * 64, row);
+                    }
+                }
+            }
+        }
+    } else if (warp == 9) {
+        // ======================================================= MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t IDESC_QK = ptx::idesc_bf16(128, 128, 0, 0);
+            constexpr uint32_t IDESC_PV = ptx::idesc_bf16(128, DP, 0, 1);
+            const uint32_t tS0 = tmem, tS1 = tmem + 128;
+            const uint32_t tO0 = tmem + 256, tO1 = tmem + 384;
+            auto issue_qk = [&](int i, int slot) {
+                const uint32_t qa = sQ + i * C::TILE_BYTES;
+                const uint32_t kb = sKV + slot * C::TILE_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < DP / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * C::CHUNK_BYTES + (kk & 3) * 32;
+                    ptx::mma_ss(i == 0 ? tS0 : tS1, ptx::smem_desc_sw128(qa + off, 16, 1024),
+                                ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
+                }
+            };
+            auto issue_pv = [&](int i, int slot, bool acc) {
+                const uint32_t vb = sKV + slot * C::TILE_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    ptx::mma_ts(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + kk * 8,
+                                ptx::smem_desc_sw128(vb + kk * 2048, C::CHUNK_BYTES, 1024), IDESC_PV,
+                                (acc || kk > 0) ? 1u : 0u);
+                }
+            };
+            ptx::mbar_wait(bar_q, 0);
+            int it = 0;
+            int slotK = it % C::NS;
+            ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
+            ++it;
+            ptx::tc_fence_after();
+            issue_qk(0, slotK);
+            ptx::mma_commit(bar_s_full0);
+            if (hasB) {
+                issue_qk(1, slotK);
+                ptx::mma_commit(bar_s_full0 + 8);
+            }
+            ptx::mma_commit(bar_kv_empty(slotK));
+            for (int j = 0; j < nst; ++j) {
+                const int slotV = it % C::NS;
+                ptx::mbar_wait(bar_kv_full(slotV), (it / C::NS) & 1);
+                ++it;
+                const bool has_next = j + 1 < nst;
+                ptx::mbar_wait(bar_p_full0, j & 1);
+                ptx::tc_fence_after();
+                issue_pv(0, slotV, j > 0);
+                if (has_next) {
+                    slotK = it % C::NS;
+                    ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
+                    ++it;
+                    ptx::tc_fence_after();
+                    issue_qk(0, slotK);
+                    ptx::mma_commit(bar_s_full0);
+                }
+                if (hasB) {
+                    ptx::mbar_wait(bar_p_full0 + 8, j & 1);
+                    ptx::tc_fence_after();
+                    issue_pv(1, slotV, j > 0);
+                }
+                ptx::mma_commit(bar_kv_empty(slotV));
+                if (has_next) {
+                    if (hasB) {
+                        issue_qk(1, slotK);
+                        ptx::mma_commit(bar_s_full0 + 8);
+                    }
+                    ptx::mma_commit(bar_kv_empty(slotK));
+                }
+            }
+            ptx::mma_commit(bar_o_full);
+        }
+    } else if (warp < 4 || hasB) {
+        // ==================================================== softmax WG i
+        const int i = warp >> 2;
+        const int wl = warp & 3;
+        const int r = threadIdx.x & 127;  // row of the sub-tile == TMEM lane
+        const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
+        const uint32_t tS = tmem + i * 128 + lane_off;
+        const uint32_t tO = tmem + 256 + i * 128 + lane_off;
+        const uint32_t bar_s = bar_s_full0 + 8 * i;
+        const uint32_t bar_p = bar_p_full0 + 8 * i;
+        const int sub = i == 0 ? subA : subB;
+
+        // ---- this row's token and its per-axis window (class-local)
+        int cc[3], sc[3];
+        class_coords(g, cls, cc);
+        sub_coords(g, sub, sc);
+        const int ub = r / BV, inner = r % BV;
+        const int u2 = ub % g.QB[2], u1 = (ub / g.QB[2]) % g.QB[1], u0 = ub / (g.QB[2] * g.QB[1]);
+        const int bx[3] = {sc[0] * g.QB[0] + u0, sc[1] * g.QB[1] + u1, sc[2] * g.QB[2] + u2};
+        const int in2 = inner & (g.B[2] - 1);
+        const int in1 = (inner >> g.logB[2]) & (g.B[1] - 1);
+        const int in0 = inner >> (g.logB[2] + g.logB[1]);
+        const int xin[3] = {in0, in1, in2};
+        int wst[3], wen[3];
+        bool valid = true;
+        for (int a = 0; a < 3; ++a) {
+            const int Lc = class_extent(g.ax[a], cc[a]);
+            int x = bx[a] * g.B[a] + xin[a];
+            if (x >= Lc) {
+                valid = false;
+                x = Lc - 1;
+            }
+            window(g.ax[a], Lc, x, &wst[a], &wen[a]);
+        }
+        const long long row_g =
+            cls_row0 + static_cast<long long>((bx[0] * g.nb[1] + bx[1]) * g.nb[2] + bx[2]) * BV + inner;
+
+        const float sl2 = p.scale_log2;
+        float m_used = -INFINITY;
+        float l_run = 0.f;
+        StageBoxes sb;
+        for (int j = 0; j < nst; ++j) {
+            decode_stage(g, lo, ext, nkv, j, KPB, sb);
+            // per-row coverage of every key of the stage; padded rows never mask
+            bool row_full = true;
+            int rlo[KPB][3], rhi[KPB][3];
+#pragma unroll
+            for (int u = 0; u < KPB; ++u) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const int base = sb.k[u][a] * g.B[a];
+                    rlo[u][a] = wst[a] - base;
+                    rhi[u][a] = sb.dead[u] ? -1 : wen[a] - base;
+                    row_full = row_full && rlo[u][a] <= 0 && rhi[u][a] >= g.B[a];
+                }
+            }
+            const bool warp_full = __all_sync(0xffffffffu, row_full || !valid);
+
+            ptx::mbar_wait(bar_s, j & 1);
+            ptx::tc_fence_after();
+            float s[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t rr[32];
+                ptx::tmem_ld32(tS + c * 32, rr);
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
+            }
+            if (!warp_full) {
+#pragma unroll
+                for (int c = 0; c < 128; ++c) {
+                    const int u = c / BV;
+                    const int in = c % BV;
+                    const int i2 = in & (g.B[2] - 1);
+                    const int i1 = (in >> g.logB[2]) & (g.B[1] - 1);
+                    const int i0 = in >> (g.logB[2] + g.logB[1]);
+                    const bool ok = i0 >= rlo[u][0] && i0 < rhi[u][0] && i1 >= rlo[u][1] && i1 < rhi[u][1] &&
+                                    i2 >= rlo[u][2] && i2 < rhi[u][2];
+                    s[c] = ok ? s[c] : -INFINITY;
+                }
+            }
+            float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+#pragma unroll
+            for (int c = 4; c < 128; c += 4) {
+                mx0 = fmaxf(mx0, s[c]);
+                mx1 = fmaxf(mx1, s[c + 1]);
+                mx2 = fmaxf(mx2, s[c + 2]);
+                mx3 = fmaxf(mx3, s[c + 3]);
+            }
+            const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+            const float m_new = fmaxf(m_used, m_tile);
+            const bool need = m_new > m_used + 8.0f;
+            if (j > 0 && __any_sync(0xffffffffu, need)) {
+                const float f = need ? ptx::ex2(m_used - m_new) : 1.0f;
+#pragma unroll
+                for (int c = 0; c < DP / 32; ++c) {
+                    uint32_t rr[32];
+                    ptx::tmem_ld32(tO + c * 32, rr);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) rr[e] = __float_as_uint(__uint_as_float(rr[e]) * f);
+                    ptx::tmem_st32(tO + c * 32, rr);
+                }
+            }
+            if (need) {
+                l_run *= ptx::ex2(m_used - m_new);
+                m_used = m_new;
+            }
+            const float neg = m_used == -INFINITY ? 0.f : -m_used;
+            float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+#pragma unroll
+            for (int c = 0; c < 128; c += 4) {
+                s[c] = ptx::ex2(fmaf(s[c], sl2, neg));
+                s[c + 1] = ptx::ex2(fmaf(s[c + 1], sl2, neg));
+                s[c + 2] = ptx::ex2(fmaf(s[c + 2], sl2, neg));
+                s[c + 3] = ptx::ex2(fmaf(s[c + 3], sl2, neg));
+                l0 += s[c];
+                l1 += s[c + 1];
+                l2 += s[c + 2];
+                l3 += s[c + 3];
+            }
+            l_run += (l0 + l1) + (l2 + l3);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t pk[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) pk[e] = ptx::pack_bf16x2(s[c * 64 + 2 * e], s[c * 64 + 2 * e + 1]);
+                ptx::tmem_st32(tS + c * 32, pk);
+            }
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(bar_p);
+        }
+
+        // ---------------------------------------------------------- epilogue
+        ptx::mbar_wait(bar_o_full, 0);
+        ptx::tc_fence_after();
+        const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
+        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o_perm) + row_g * DP;
+#pragma unroll
+        for (int c = 0; c < DP / 32; ++c) {
+            uint32_t rr[32];
+            ptx::tmem_ld32(tO + c * 32, rr);
+            ptx::tmem_wait_ld();
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+                pk[e] = ptx::pack_bf16x2(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
+            if (valid) {
+                uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            }
+        }
+        if (valid) {
+            const float m_eff = m_used == -INFINITY ? 0.f : m_used;
+            p.lse_perm[row_g] = (m_eff + __log2f(l_run)) * 0.69314718055994530942f;
+        }
+        ptx::tc_fence_before();
+    }
+
+    __syncthreads();
+    if (warp == 8) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
+template <int DP, int BV>
+static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                            const CUtensorMap& tv, long long n_ctas, cudaStream_t stream) {
+    using C = Cfg<DP, BV>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gna_attn_sm100<DP, BV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    if (n_ctas <= 0) return cudaSuccess;
+    gna_attn_sm100<DP, BV><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, long long n_ctas, cudaStream_t stream) {
+    const int dp = p.g.Dp, bv = p.g.box_vol;
+    if (dp == 128 && bv == 128) return launch_t<128, 128>(p, tq, tk, tv, n_ctas, stream);
+    if (dp == 128 && bv == 64) return launch_t<128, 64>(p, tq, tk, tv, n_ctas, stream);
+    if (dp == 64 && bv == 128) return launch_t<64, 128>(p, tq, tk, tv, n_ctas, stream);
+    if (dp == 64 && bv == 64) return launch_t<64, 64>(p, tq, tk, tv, n_ctas, stream);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace gna

@@ -1,0 +1,40 @@
+// kernels.h -- launch interface between the host runtime (api.cu) and the
+// sm_100a kernels.  Product-path code; independent of oracle/.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "geom.cuh"
+
+namespace gna {
+
+struct AttnParams {
+    Geometry g;
+    const int4* items;      // work list: {class, subA, subB (-1 none), kv boxes}
+    long long n_items;      // items per (batch, head)
+    long long work_begin;   // global work index offset of blockIdx.x == 0
+    void* o_perm;           // bf16 permuted O  [BH][C][nbox][box_vol][Dp]
+    float* lse_perm;        // fp32 permuted LSE [BH][C][nbox][box_vol]
+    float scale_log2;       // softmax scale * log2(e)
+};
+
+// Permuted layout sizes (rows of Dp elements)
+inline long long perm_rows(const Geometry& g) {
+    return static_cast<long long>(g.batch) * g.heads * g.ncls * g.nbox * g.box_vol;
+}
+
+cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                             const CUtensorMap& tv, long long n_ctas, cudaStream_t stream);
+
+// q/k/v natural [B][s0][s1][s2][H][D] -> permuted [BH][C][nbox][box_vol][Dp]
+cudaError_t launch_permute_qkv(const Geometry& g, const void* q, const void* k, const void* v, void* qp,
+                               void* kp, void* vp, cudaStream_t stream);
+// permuted O / LSE -> natural layout (crop padding)
+cudaError_t launch_unpermute(const Geometry& g, const void* op, const float* lsep, void* out, float* lse,
+                             cudaStream_t stream);
+
+cudaError_t launch_debug_windows(const Geometry& g, int32_t* dev_out, cudaStream_t stream);
+cudaError_t launch_debug_visits(const Geometry& g, int32_t* dev_out, cudaStream_t stream);
+
+}  // namespace gna
