@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""bench.py -- GNA forward on B200: effective TFLOP/s (kept-pair FLOPs only),
+speedup over the same kernel run densely, against the NATTENSim bound.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
+
+A step = one pass of the hot path over one batch: permute Q,K,V -> fused
+attention (analytic tile ranges, tcgen05 mainloop, O+LSE epilogue) -> inverse
+permute, inputs resident in HBM, L2 flushed (256 MiB write) between timed
+steps outside the events.  Multi-GPU (torchrun): weak scaling, every rank runs
+its own shard (batch x heads units) of a global batch N x B; no collective on
+the data path; times are the max over ranks.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from gna_inputs import SEED, WORKLOADS, make_qkv, sample_rows  # noqa: E402
+
+DEFAULT_WORKLOAD = "c2b_flux64_s16"
+METRIC = "GNA fwd effective TFLOP/s (bf16) and speedup vs dense FMHA vs simulator bound"
+
+
+def _peaks():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return mp.get("bf16_tflops", 1590.0), mp.get("bf16_tflops_sustained", 1400.0), mp.get("hbm_gbs", 6650.0), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms in the background."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    import torch.distributed as dist
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1 and not dist.is_initialized():
+        import torch
+
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend)
+    return ws, rank, local
+
+
+def _max_over_ranks(vals, ws, device):
+    if ws == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def cpu_oracle_sample(w, budget_s, seed_offset=0):
+    """Time the fp64 oracle (as it stands) on a bounded random row sample of the
+    workload; returns (TFLOP/s, seconds, rows, cores)."""
+    import numpy as np
+
+    import oracle as O
+    from gna_inputs import as_f32_numpy
+
+    f = w.full()
+    p = O.Params(f["spatial"], f["window"], f["stride"], f["dilation"], f["causal"])
+    q, k, v = make_qkv(w.batch, w.spatial, w.heads, w.head_dim, seed=SEED + seed_offset)
+    qn, kn, vn = as_f32_numpy(q), as_f32_numpy(k), as_f32_numpy(v)
+    cores = O.num_threads()
+    n = max(cores, 8)
+    total_pairs, total_t, total_rows = 0, 0.0, 0
+    rng_seed = SEED + 7
+    while total_t < budget_s:
+        rows = sample_rows(w.batch, w.spatial, w.heads, n, seed=rng_seed)
+        rng_seed += 1
+        t0 = time.perf_counter()
+        _, _, pairs = O.forward_rows(qn, kn, vn, p, rows)
+        dt = time.perf_counter() - t0
+        total_pairs += pairs
+        total_t += dt
+        total_rows += n
+        if dt < budget_s / 8:
+            n *= 2
+    tflops = 4.0 * w.head_dim * total_pairs / total_t / 1e12
+    return tflops, total_t, total_rows, cores
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the fp64 CPU oracle on the host cores (bounded samples)."""
+    if rank != 0:
+        return
+    w = WORKLOADS[args.workload]
+    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_oracle_sample(w, budget / 4)
+    vals, secs, rows_tot = [], 0.0, 0
+    cores = 1
+    for _ in range(args.steps):
+        v, t, r, cores = cpu_oracle_sample(w, budget)
+        vals.append(v)
+        secs += t
+        rows_tot += r
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * secs / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "spatial": list(w.spatial), "window": list(w.window),
+                   "stride": list(w.stride), "heads": w.heads, "head_dim": w.head_dim, "batch": w.batch},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{rows_tot} random (b, token, h) rows of {w.name}, fp64, ~{budget:.0f} s per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _traffic_from_profiles(workload):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(workload, {}).get("attention_dram_bytes")
+    except Exception:
+        return None
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+
+    import paper_2504_16922_b200 as gna
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = WORKLOADS[args.workload]
+    f = w.full()
+    B, H, D = w.batch, w.heads, w.head_dim
+    # weak scaling: rank r owns units [r*B*H, (r+1)*B*H) of a global batch N*B
+    qh, kh, vh = make_qkv(B, w.spatial, H, D, seed=SEED + 1000 * rank)
+    qh, kh, vh = (t.pin_memory() for t in (qh, kh, vh))
+    q, k, v = (t.to(dev) for t in (qh, kh, vh))
+    out = torch.empty_like(q)
+    lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=dev)
+    info = gna.plan_info(B, H, D, **f)
+    eff_flops = 4.0 * D * info["kept_pairs"] * B * H
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    win, st, dil, cau = f["window"], f["stride"], f["dilation"], f["causal"]
+
+    def fwd():
+        gna.forward(q, k, v, win, st, dil, cau, out=out, lse=lse)
+
+    def timed(fn, steps):
+        ts = []
+        for _ in range(steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return ts
+
+    for _ in range(max(3, args.warmup)):
+        fwd()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K full steps (value), clocks sampled around it
+    with ClockSampler(local) as clk:
+        t_soak = time.time()
+        while time.time() - t_soak < 0.4:
+            fwd()
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        step_ms = timed(fwd, args.steps)
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        t_soak = time.time()
+        while time.time() - t_soak < 0.3:
+            fwd()
+        torch.cuda.synchronize()
+    total_ms = sum(step_ms)
+
+    # ---- per-stage times (same stream, events between the three launches)
+    stage = {"permute": [], "attention": [], "unpermute": []}
+    o2 = torch.empty_like(q)
+    l2 = torch.empty_like(lse)
+    for _ in range(args.steps):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        gna.permute(q, k, v, o2, win, st, dil, cau)
+        ev[1].record(stream)
+        gna.attention_permuted(q, k, v, o2, win, st, dil, cau)
+        ev[2].record(stream)
+        gna.unpermute(q, k, v, o2, l2, win, st, dil, cau)
+        ev[3].record(stream)
+        ev[3].synchronize()
+        for i, kname in enumerate(stage):
+            stage[kname].append(ev[i].elapsed_time(ev[i + 1]))
+
+    # ---- dense baseline: same kernel, window = extent, same box (a6)
+    dense_win = tuple(w.spatial)
+    ones = tuple(1 for _ in w.spatial)
+    gna.forward(q, k, v, dense_win, ones, None, None, out=o2, lse=l2, box=info["box"])
+    gna.permute(q, k, v, o2, dense_win, ones, box=info["box"])
+    dense_ms = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gna.attention_permuted(q, k, v, o2, dense_win, ones, box=info["box"])
+        e1.record(stream)
+        e1.synchronize()
+        dense_ms.append(e0.elapsed_time(e1))
+
+    # ---- end to end through the public API with host buffers (pinned)
+    out_h = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    lse_h = torch.empty(lse.shape, dtype=lse.dtype, pin_memory=True)
+    e2e_ms = []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        q.copy_(qh, non_blocking=True)
+        k.copy_(kh, non_blocking=True)
+        v.copy_(vh, non_blocking=True)
+        fwd()
+        out_h.copy_(out, non_blocking=True)
+        lse_h.copy_(lse, non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+
+    att_ms = statistics.mean(stage["attention"])
+    vals = _max_over_ranks([total_ms, sum(e2e_ms), att_ms, statistics.mean(dense_ms)], ws, dev)
+    total_ms, e2e_total, att_ms_max, dense_max = vals
+    if rank != 0:
+        return
+
+    peak_burst, peak_sus, hbm, peak_kind = _peaks()
+    ms_per_step = total_ms / args.steps
+    value = ws * eff_flops / (ms_per_step * 1e-3) / 1e12
+    e2e_value = ws * eff_flops / (e2e_total / args.steps * 1e-3) / 1e12
+    achieved = eff_flops / (att_ms * 1e-3) / 1e12
+    mma_flops = 4.0 * D * 128 * 128 * info["kv_stages_total"] * B * H  # issued tensor work (both GEMMs)
+    n_tok = w.n_tokens
+    nat_bytes = B * n_tok * H * D * 2
+    perm_bytes = 6 * nat_bytes  # read q,k,v + write permuted q,k,v (algorithmic, no padding)
+    unperm_bytes = 2 * nat_bytes + 2 * B * n_tok * H * 4
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        cv, ct, cr, cores = cpu_oracle_sample(w, args.cpu_budget)
+        cpu = {"value": cv, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+               "sample": f"{cr} random (b, token, h) rows of {w.name} (fp64 oracle, {ct:.1f} s)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": w.name, "spatial": list(w.spatial), "window": list(w.window), "stride": list(w.stride),
+                   "dilation": list(f["dilation"]), "causal": [int(c) for c in f["causal"]], "heads": H,
+                   "head_dim": D, "batch_per_gpu": B, "global_batch": B * ws,
+                   "parallelism": f"batchxheads x{ws}", "l2": "flushed (256 MiB write) between timed steps",
+                   "box": info["box"], "q_sub": info["q_sub"]},
+        "speedup_vs_dense": dense_max / att_ms_max,
+        "bound": info["bound"],
+        "speedup_frac_of_bound": (dense_max / att_ms_max) / info["bound"],
+        "flopwise_speedup": float(n_tok * n_tok) / info["kept_pairs"] if not any(f["causal"]) else None,
+        "stages_ms": {k2: statistics.mean(v2) for k2, v2 in stage.items()},
+        "dense_attention_ms": statistics.mean(dense_ms),
+        "dense_effective_tflops": 4.0 * D * n_tok * n_tok * B * H / (statistics.mean(dense_ms) * 1e-3) / 1e12,
+        "permute_gbs": perm_bytes / (statistics.mean(stage["permute"]) * 1e-3) / 1e9,
+        "unpermute_gbs": unperm_bytes / (statistics.mean(stage["unpermute"]) * 1e-3) / 1e9,
+        "mma_issued_tflops": mma_flops / (att_ms * 1e-3) / 1e12,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
+                     "frac": achieved / peak_burst, "traffic": _traffic_from_profiles(w.name),
+                     "kernel": "gna_attn_sm100", "peak_kind": f"{peak_kind} bf16 burst",
+                     "frac_of_sustained": achieved / peak_sus},
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": 3 * nat_bytes,
+                "d2h_bytes_per_step": nat_bytes + B * n_tok * H * 4},
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "context": {"paper_gna_pflops_fp16": 1.3, "paper_e2e_speedups": "28%-46% (P:72)"},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
