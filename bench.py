@@ -312,7 +312,7 @@ def run_ours(args, ws, rank, local):
     value = ws * eff_flops / (ms_per_step * 1e-3) / 1e12
     e2e_value = ws * eff_flops / (e2e_total / args.steps * 1e-3) / 1e12
     achieved = eff_flops / (att_ms * 1e-3) / 1e12
-    mma_flops = 4.0 * D * 128 * 128 * info["kv_stages_total"] * B * H  # issued tensor work (both GEMMs)
+    mma_flops = 4.0 * info["padded_head_dim"] * 128 * 128 * info["subtile_stages"] * B * H  # issued (both GEMMs)
     n_tok = w.n_tokens
     nat_bytes = B * n_tok * H * D * 2
     perm_bytes = 6 * nat_bytes  # read q,k,v + write permuted q,k,v (algorithmic, no padding)

@@ -100,6 +100,8 @@ typedef struct gna_plan_info_t {
     long long n_work;       /* n_items * batch * heads */
     long long n_paired;     /* items with two Q sub-tiles */
     long long kv_stages_total; /* sum over items of 128-row KV stages visited */
+    long long subtile_stages;  /* sum over items of stages x Q sub-tiles (MMA work units:
+                                  one unit = 128x128 QK^T + 128x128 PV per head_dim) */
     long long visited_max;  /* max KV boxes visited by one work item */
     long long dense_boxes;  /* KV boxes per class covering all keys */
     double bound;           /* NATTENSim bound at these tiles: dense / visited_max */

@@ -147,7 +147,7 @@ Geometry make_geometry(const gna_args* a, const int B[3], const int QB[3]) {
 struct Built {
     std::vector<int4> items;
     double cost = 0;
-    long long stages = 0, paired = 0, vmax = 0;
+    long long stages = 0, paired = 0, vmax = 0, sub_stages = 0;
 };
 
 constexpr double kSingleCost = 1.3;  // relative cost of a 128-row CTA stage vs a paired one (2.0)
@@ -215,6 +215,7 @@ Built build_items(const Geometry& g) {
         it.w = static_cast<int>(nbx);
         const long long st = (nbx + kpb - 1) / kpb;
         out.stages += st;
+        out.sub_stages += st * (it.z >= 0 ? 2 : 1);
         out.vmax = std::max(out.vmax, nbx);
         if (it.z >= 0) ++out.paired;
         out.cost += (it.z >= 0 ? 2.0 : kSingleCost) * st;
@@ -314,6 +315,7 @@ std::shared_ptr<Plan> get_plan(const gna_args* a) {
             in.n_items = static_cast<long long>(plan->items.size());
             in.n_paired = b.paired;
             in.kv_stages_total = b.stages;
+            in.subtile_stages = b.sub_stages;
             in.visited_max = b.vmax;
             long long dense = 1;
             for (int ax = 0; ax < 3; ++ax) dense *= ceil_div(ceil_div(a->spatial[ax], a->dilation[ax]), g.B[ax]);

@@ -5,11 +5,12 @@
 // the sub-tiles' analytic ranges (geom.cuh; §3.3): no mask tensor
 // ever exists in HBM, and boxes outside the range are never loaded.
 //
-// Warp roles (320 threads):
-//   warps 0-3  softmax WG0 : rows of sub-tile A, TMEM lanes 0-127, S0/P0, O0
-//   warps 4-7  softmax WG1 : rows of sub-tile B, S1/P1, O1
-//   warp  8    TMA producer: Q sub-tiles once, then K_j, V_j into a smem ring
+// Warp roles (384 threads, registers re-balanced with setmaxnreg):
+//   warps 0-3  softmax WG0 : rows of sub-tile A, TMEM lanes 0-127, S0/P0, O0 (224 regs)
+//   warps 4-7  softmax WG1 : rows of sub-tile B, S1/P1, O1                   (224 regs)
+//   warp  8    TMA producer: Q sub-tiles once, then K_j, V_j into a smem ring (64 regs)
 //   warp  9    MMA issuer  : tcgen05.mma, one elected lane
+//   warps 10-11 idle (complete the control warpgroup for setmaxnreg)
 // TMEM (512 columns x 128 lanes, fp32):  S0 [0,128)  S1 [128,256)
 //   O0 [256, 256+Dp)  O1 [384, 384+Dp); P_i (bf16x2) aliases S_i's first 64.
 //
@@ -49,7 +50,7 @@ struct Cfg {
     static constexpr int KV_OFF = 2 * TILE_BYTES;
     static constexpr int BAR_OFF = KV_OFF + NS * TILE_BYTES;
     static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
-    static constexpr int THREADS = 320;
+    static constexpr int THREADS = 384;
 };
 
 struct StageBoxes {
@@ -74,10 +75,50 @@ __device__ __forceinline__ void decode_stage(const Geometry& g, const int lo[3],
     }
 }
 
+// ---- separable GNA mask of one row over one box, as a bit mask over the
+// box's rows (row-major (i0, i1, i2)).  Axis intervals [lo, hi) are relative
+// to the box origin.  Built from per-axis interval masks by multiplying with
+// "comb" constants (no carries: the operands occupy disjoint bit fields).
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ u128 bits_below(int n) {  // n in [0, 128]
+    return n >= 128 ? ~static_cast<u128>(0) : ((static_cast<u128>(1) << n) - 1);
+}
+__device__ __forceinline__ u128 bit_range(int a, int b) { return bits_below(b) & ~bits_below(a); }
+
+struct BoxMaskConsts {
+    u128 comb1;  // bit i1*B2 for i1 < B1
+    u128 comb0;  // bit i0*B1*B2 for i0 < B0
+};
+
+__device__ __forceinline__ BoxMaskConsts box_mask_consts(const Geometry& g) {
+    BoxMaskConsts c;
+    c.comb1 = 0;
+    c.comb0 = 0;
+    for (int i = 0; i < g.B[1]; ++i) c.comb1 |= static_cast<u128>(1) << (i * g.B[2]);
+    for (int i = 0; i < g.B[0]; ++i) c.comb0 |= static_cast<u128>(1) << (i * g.B[1] * g.B[2]);
+    return c;
+}
+
+__device__ __forceinline__ u128 box_row_mask(const Geometry& g, const BoxMaskConsts& mc, const int lo[3],
+                                             const int hi[3]) {
+    int a[3], b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a[k] = max(lo[k], 0);
+        b[k] = min(hi[k], g.B[k]);
+        if (a[k] >= b[k]) return 0;
+    }
+    const u128 m2 = bit_range(a[2], b[2]);
+    const u128 m12 = (m2 * mc.comb1) & bit_range(a[1] * g.B[2], b[1] * g.B[2]);
+    const int s01 = g.B[1] * g.B[2];
+    return (m12 * mc.comb0) & bit_range(a[0] * s01, b[0] * s01);
+}
+
 }  // namespace
 
 template <int DP, int BV>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(384, 1)
     gna_attn_sm100(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v) {
     using C = Cfg<DP, BV>;
@@ -150,7 +191,9 @@ __global__ void __launch_bounds__(320, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
-    if (warp == 8) {
+    if (warp >= 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+      if (warp == 8) {
         // ===================================================== TMA producer
         if (lane == 0) {
             ptx::tma_prefetch_desc(&tmap_q);
@@ -261,7 +304,10 @@ __global__ void __launch_bounds__(320, 1)
             }
             ptx::mma_commit(bar_o_full);
         }
-    } else if (warp < 4 || hasB) {
+      }
+    } else {
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+      if (warp < 4 || hasB) {
         // ==================================================== softmax WG i
         const int i = warp >> 2;
         const int wl = warp & 3;
@@ -298,6 +344,7 @@ __global__ void __launch_bounds__(320, 1)
         const long long row_g =
             cls_row0 + static_cast<long long>((bx[0] * g.nb[1] + bx[1]) * g.nb[2] + bx[2]) * BV + inner;
 
+        const BoxMaskConsts mconst = box_mask_consts(g);
         const float sl2 = p.scale_log2;
         float m_used = -INFINITY;
         float l_run = 0.f;
@@ -331,17 +378,13 @@ __global__ void __launch_bounds__(320, 1)
                 for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
             }
             if (!warp_full) {
+                // 128-bit row mask of the stage (1 or 2 boxes), then one select per element
+                u128 m = box_row_mask(g, mconst, rlo[0], rhi[0]);
+                if (KPB == 2) m |= box_row_mask(g, mconst, rlo[KPB - 1], rhi[KPB - 1]) << 64;
+                const uint32_t mw[4] = {static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32),
+                                        static_cast<uint32_t>(m >> 64), static_cast<uint32_t>(m >> 96)};
 #pragma unroll
-                for (int c = 0; c < 128; ++c) {
-                    const int u = c / BV;
-                    const int in = c % BV;
-                    const int i2 = in & (g.B[2] - 1);
-                    const int i1 = (in >> g.logB[2]) & (g.B[1] - 1);
-                    const int i0 = in >> (g.logB[2] + g.logB[1]);
-                    const bool ok = i0 >= rlo[u][0] && i0 < rhi[u][0] && i1 >= rlo[u][1] && i1 < rhi[u][1] &&
-                                    i2 >= rlo[u][2] && i2 < rhi[u][2];
-                    s[c] = ok ? s[c] : -INFINITY;
-                }
+                for (int c = 0; c < 128; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
             }
             float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
 #pragma unroll
@@ -421,10 +464,12 @@ __global__ void __launch_bounds__(320, 1)
             p.lse_perm[row_g] = (m_eff + __log2f(l_run)) * 0.69314718055994530942f;
         }
         ptx::tc_fence_before();
+      }
     }
 
     __syncthreads();
     if (warp == 8) {
+        __syncwarp();
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, 512);
     }

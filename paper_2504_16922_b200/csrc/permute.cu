@@ -21,117 +21,142 @@ namespace gna {
 
 namespace {
 
-struct PermIndex {
-    // decodes a permuted row into (bh, token offset in the natural layout) or invalid
-    __device__ __forceinline__ static bool decode(const Geometry& g, long long row, long long* nat_row) {
-        const int inner = static_cast<int>(row % g.box_vol);
-        long long t = row / g.box_vol;
-        const int blin = static_cast<int>(t % g.nbox);
-        t /= g.nbox;
-        const int cls = static_cast<int>(t % g.ncls);
-        const long long bh = t / g.ncls;
-        const int b = static_cast<int>(bh / g.heads), h = static_cast<int>(bh % g.heads);
-        int cc[3];
-        class_coords(g, cls, cc);
-        const int bxs[3] = {blin / (g.nb[1] * g.nb[2]), (blin / g.nb[2]) % g.nb[1], blin % g.nb[2]};
-        const int in[3] = {inner >> (g.logB[2] + g.logB[1]), (inner >> g.logB[2]) & (g.B[1] - 1),
-                           inner & (g.B[2] - 1)};
-        long long tok = 0;
-        for (int a = 0; a < 3; ++a) {
-            const int x = bxs[a] * g.B[a] + in[a];
-            if (x >= class_extent(g.ax[a], cc[a])) return false;
-            tok = tok * g.ax[a].L + (cc[a] + g.ax[a].d * x);
-        }
-        const long long N = static_cast<long long>(g.ax[0].L) * g.ax[1].L * g.ax[2].L;
-        *nat_row = ((static_cast<long long>(b) * N + tok) * g.heads + h);
-        return true;
-    }
+// One work unit = one box (box_vol token rows) of one (tensor, batch*head,
+// class).  The unit is decoded once per CTA (uniform), rows only need shifts.
+struct BoxUnit {
+    long long perm_row0;   // first row of the box in the permuted tensor
+    long long nat_base;    // b * N * H + h  (natural row = nat_base + tok * H)
+    int bx[3], cc[3], Lc[3];
 };
 
-// grid.y = tensor index (0..2).  Vectors of 8 bf16 (16 B).
+__device__ __forceinline__ BoxUnit decode_unit(const Geometry& g, long long u /* (cls, blin, bh) */) {
+    BoxUnit r;
+    const long long BH = static_cast<long long>(g.batch) * g.heads;
+    const long long bh = u % BH;
+    const long long cb = u / BH;
+    const int blin = static_cast<int>(cb % g.nbox);
+    const int cls = static_cast<int>(cb / g.nbox);
+    class_coords(g, cls, r.cc);
+    r.bx[0] = blin / (g.nb[1] * g.nb[2]);
+    r.bx[1] = (blin / g.nb[2]) % g.nb[1];
+    r.bx[2] = blin % g.nb[2];
+    for (int a = 0; a < 3; ++a) r.Lc[a] = class_extent(g.ax[a], r.cc[a]);
+    r.perm_row0 = ((bh * g.ncls + cls) * static_cast<long long>(g.nbox) + blin) * g.box_vol;
+    const long long N = static_cast<long long>(g.ax[0].L) * g.ax[1].L * g.ax[2].L;
+    const long long b = bh / g.heads, h = bh % g.heads;
+    r.nat_base = b * N * g.heads + h;
+    return r;
+}
+
+// natural row of box row `inner`, or -1 for a padding row
+__device__ __forceinline__ long long nat_row(const Geometry& g, const BoxUnit& u, int inner) {
+    const int in0 = inner >> (g.logB[2] + g.logB[1]);
+    const int in1 = (inner >> g.logB[2]) & (g.B[1] - 1);
+    const int in2 = inner & (g.B[2] - 1);
+    const int x0 = u.bx[0] * g.B[0] + in0, x1 = u.bx[1] * g.B[1] + in1, x2 = u.bx[2] * g.B[2] + in2;
+    if (x0 >= u.Lc[0] || x1 >= u.Lc[1] || x2 >= u.Lc[2]) return -1;
+    const long long t0 = u.cc[0] + static_cast<long long>(g.ax[0].d) * x0;
+    const long long t1 = u.cc[1] + g.ax[1].d * x1;
+    const long long t2 = u.cc[2] + g.ax[2].d * x2;
+    const long long tok = (t0 * g.ax[1].L + t1) * g.ax[2].L + t2;
+    return u.nat_base + tok * g.heads;
+}
+
+// grid-stride over units (tensor, cls, box, bh); VPR = Dp/8 16-byte vectors per permuted row.
+template <int VPR, int BV>
 __global__ void __launch_bounds__(256) permute_qkv_kernel(Geometry g, const uint4* __restrict__ q,
                                                           const uint4* __restrict__ k, const uint4* __restrict__ v,
                                                           uint4* __restrict__ qp, uint4* __restrict__ kp,
-                                                          uint4* __restrict__ vp, long long rows) {
-    const uint4* src = blockIdx.y == 0 ? q : (blockIdx.y == 1 ? k : v);
-    uint4* dst = blockIdx.y == 0 ? qp : (blockIdx.y == 1 ? kp : vp);
-    const int vpr_out = g.Dp / 8;  // vectors per permuted row
-    const int vpr_in = g.D / 8;    // vectors per natural row (D >= 8 assumed, D % 8 == 0)
-    const long long total = rows * vpr_out;
-    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long row = idx / vpr_out;
-        const int vcol = static_cast<int>(idx % vpr_out);
-        long long nat;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (vcol < vpr_in && PermIndex::decode(g, row, &nat)) val = __ldg(src + nat * vpr_in + vcol);
-        dst[idx] = val;
+                                                          uint4* __restrict__ vp, long long units_per_tensor) {
+    constexpr int RPP = 256 / VPR;  // rows per pass
+    constexpr int NP = BV / RPP;    // passes per box
+    const int vcol = threadIdx.x % VPR;
+    const int r0 = threadIdx.x / VPR;
+    const int vin = g.D / 8;
+    for (long long unit = blockIdx.x; unit < 3 * units_per_tensor; unit += gridDim.x) {
+        const int t = static_cast<int>(unit / units_per_tensor);
+        const BoxUnit u = decode_unit(g, unit % units_per_tensor);
+        const uint4* src = t == 0 ? q : (t == 1 ? k : v);
+        uint4* dst = t == 0 ? qp : (t == 1 ? kp : vp);
+        uint4 val[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const long long nr = nat_row(g, u, r0 + p * RPP);
+            val[p] = (nr >= 0 && vcol < vin) ? __ldg(src + nr * vin + vcol) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) dst[(u.perm_row0 + r0 + p * RPP) * VPR + vcol] = val[p];
     }
 }
 
-// natural-order walk over (b, token, h) rows; reads scattered permuted rows.
+template <int VPR, int BV>
 __global__ void __launch_bounds__(256) unpermute_kernel(Geometry g, const uint4* __restrict__ op,
                                                         const float* __restrict__ lsep, uint4* __restrict__ out,
-                                                        float* __restrict__ lse, long long nat_rows) {
-    const int vpr_in = g.Dp / 8;
-    const int vpr_out = g.D / 8;
-    const long long total = nat_rows * vpr_out;
-    const long long N = static_cast<long long>(g.ax[0].L) * g.ax[1].L * g.ax[2].L;
-    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long nat = idx / vpr_out;
-        const int vcol = static_cast<int>(idx % vpr_out);
-        const int h = static_cast<int>(nat % g.heads);
-        const long long bt = nat / g.heads;
-        const long long tok = bt % N;
-        const int b = static_cast<int>(bt / N);
-        const int t2 = static_cast<int>(tok % g.ax[2].L);
-        const int t1 = static_cast<int>((tok / g.ax[2].L) % g.ax[1].L);
-        const int t0 = static_cast<int>(tok / (static_cast<long long>(g.ax[2].L) * g.ax[1].L));
-        const int t[3] = {t0, t1, t2};
-        int cls = 0, blin = 0, inner = 0;
-        for (int a = 0; a < 3; ++a) {
-            const int c = t[a] % g.ax[a].d, x = t[a] / g.ax[a].d;
-            cls = cls * g.ax[a].d + c;
-            blin = blin * g.nb[a] + (x >> g.logB[a]);
-            inner = (inner << g.logB[a]) | (x & (g.B[a] - 1));
+                                                        float* __restrict__ lse, long long units) {
+    constexpr int RPP = 256 / VPR;
+    constexpr int NP = BV / RPP;
+    const int vcol = threadIdx.x % VPR;
+    const int r0 = threadIdx.x / VPR;
+    const int vout = g.D / 8;
+    for (long long unit = blockIdx.x; unit < units; unit += gridDim.x) {
+        const BoxUnit u = decode_unit(g, unit);
+        uint4 val[NP];
+        float lv[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const long long pr = u.perm_row0 + r0 + p * RPP;
+            val[p] = __ldg(op + pr * VPR + vcol);
+            lv[p] = vcol == 0 ? __ldg(lsep + pr) : 0.f;
         }
-        const long long prow =
-            ((static_cast<long long>(b) * g.heads + h) * g.ncls + cls) * static_cast<long long>(g.nbox) * g.box_vol +
-            static_cast<long long>(blin) * g.box_vol + inner;
-        out[idx] = __ldg(op + prow * vpr_in + vcol);
-        if (vcol == 0 && lse != nullptr) lse[nat] = __ldg(lsep + prow);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            const long long nr = nat_row(g, u, r0 + p * RPP);
+            if (nr < 0) continue;
+            if (vcol < vout) out[nr * vout + vcol] = val[p];
+            if (vcol == 0 && lse != nullptr) lse[nr] = lv[p];
+        }
     }
 }
 
-int grid_for(long long work) {
+int grid_for(long long units) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    long long blocks = (work + 255) / 256;
     const long long cap = static_cast<long long>(sms) * 8;  // 8 x 256 threads resident per SM
-    return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+    return static_cast<int>(units < cap ? (units > 0 ? units : 1) : cap);
 }
 
 }  // namespace
 
 cudaError_t launch_permute_qkv(const Geometry& g, const void* q, const void* k, const void* v, void* qp, void* kp,
                                void* vp, cudaStream_t stream) {
-    const long long rows = perm_rows(g);
-    const long long work = rows * (g.Dp / 8);
-    dim3 grid(grid_for(work), 3);
-    permute_qkv_kernel<<<grid, 256, 0, stream>>>(g, static_cast<const uint4*>(q), static_cast<const uint4*>(k),
-                                                 static_cast<const uint4*>(v), static_cast<uint4*>(qp),
-                                                 static_cast<uint4*>(kp), static_cast<uint4*>(vp), rows);
+    const long long units = static_cast<long long>(g.batch) * g.heads * g.ncls * g.nbox;
+    const int grid = grid_for(3 * units);
+    auto args = [&](auto kern) {
+        kern<<<grid, 256, 0, stream>>>(g, static_cast<const uint4*>(q), static_cast<const uint4*>(k),
+                                       static_cast<const uint4*>(v), static_cast<uint4*>(qp), static_cast<uint4*>(kp),
+                                       static_cast<uint4*>(vp), units);
+    };
+    if (g.Dp == 128 && g.box_vol == 128) args(permute_qkv_kernel<16, 128>);
+    else if (g.Dp == 128 && g.box_vol == 64) args(permute_qkv_kernel<16, 64>);
+    else if (g.Dp == 64 && g.box_vol == 128) args(permute_qkv_kernel<8, 128>);
+    else if (g.Dp == 64 && g.box_vol == 64) args(permute_qkv_kernel<8, 64>);
+    else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
 cudaError_t launch_unpermute(const Geometry& g, const void* op, const float* lsep, void* out, float* lse,
                              cudaStream_t stream) {
-    const long long nat_rows = static_cast<long long>(g.batch) * g.ax[0].L * g.ax[1].L * g.ax[2].L * g.heads;
-    const long long work = nat_rows * (g.D / 8);
-    unpermute_kernel<<<grid_for(work), 256, 0, stream>>>(g, static_cast<const uint4*>(op), lsep,
-                                                          static_cast<uint4*>(out), lse, nat_rows);
+    const long long units = static_cast<long long>(g.batch) * g.heads * g.ncls * g.nbox;
+    const int grid = grid_for(units);
+    auto args = [&](auto kern) {
+        kern<<<grid, 256, 0, stream>>>(g, static_cast<const uint4*>(op), lsep, static_cast<uint4*>(out), lse, units);
+    };
+    if (g.Dp == 128 && g.box_vol == 128) args(unpermute_kernel<16, 128>);
+    else if (g.Dp == 128 && g.box_vol == 64) args(unpermute_kernel<16, 64>);
+    else if (g.Dp == 64 && g.box_vol == 128) args(unpermute_kernel<8, 128>);
+    else if (g.Dp == 64 && g.box_vol == 64) args(unpermute_kernel<8, 64>);
+    else return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 

@@ -41,7 +41,8 @@ class GnaPlanInfo(ctypes.Structure):
         ("box", _I3), ("q_sub", _I3), ("box_vol", ctypes.c_int), ("padded_head_dim", ctypes.c_int),
         ("n_classes", ctypes.c_int), ("n_boxes_per_class", ctypes.c_int),
         ("n_items", ctypes.c_longlong), ("n_work", ctypes.c_longlong), ("n_paired", ctypes.c_longlong),
-        ("kv_stages_total", ctypes.c_longlong), ("visited_max", ctypes.c_longlong),
+        ("kv_stages_total", ctypes.c_longlong), ("subtile_stages", ctypes.c_longlong),
+        ("visited_max", ctypes.c_longlong),
         ("dense_boxes", ctypes.c_longlong), ("bound", ctypes.c_double), ("kept_pairs", ctypes.c_longlong),
         ("workspace_bytes", ctypes.c_size_t),
     ]
