@@ -8,7 +8,7 @@
 // Warp roles (384 threads, registers re-balanced with setmaxnreg):
 //   warps 0-3  softmax WG0 : rows of sub-tile A, TMEM lanes 0-127, S0/P0, O0 (224 regs)
 //   warps 4-7  softmax WG1 : rows of sub-tile B, S1/P1, O1                   (224 regs)
-//   warp  8    TMA producer: Q sub-tiles once, then K_j, V_j into a smem ring (64 regs)
+//   warp  8    TMA producer: Q sub-tiles once, then K_j, V_j into a smem ring (56 regs)
 //   warp  9    MMA issuer  : tcgen05.mma, one elected lane
 //   warps 10-11 idle (complete the control warpgroup for setmaxnreg)
 // TMEM (512 columns x 128 lanes, fp32):  S0 [0,128)  S1 [128,256)
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     } else {
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
       if (warp < 4 || hasB) {
         // ==================================================== softmax WG i
         const int i = warp >> 2;
