@@ -388,13 +388,13 @@ __global__ void __launch_bounds__(384, 1)
             }
             float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
 #pragma unroll
-            for (int c = 4; c < 128; c += 4) {
-                mx0 = fmaxf(mx0, s[c]);
-                mx1 = fmaxf(mx1, s[c + 1]);
-                mx2 = fmaxf(mx2, s[c + 2]);
-                mx3 = fmaxf(mx3, s[c + 3]);
+            for (int c = 4; c < 128; c += 8) {
+                mx0 = ptx::max3(mx0, s[c], s[c + 1]);
+                mx1 = ptx::max3(mx1, s[c + 2], s[c + 3]);
+                mx2 = ptx::max3(mx2, s[c + 4], s[c + 5]);
+                mx3 = ptx::max3(mx3, s[c + 6], s[c + 7]);
             }
-            const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+            const float m_tile = ptx::max3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
             const float m_new = fmaxf(m_used, m_tile);
             const bool need = m_new > m_used + 8.0f;
             if (j > 0 && __any_sync(0xffffffffu, need)) {
@@ -414,26 +414,27 @@ __global__ void __launch_bounds__(384, 1)
                 m_used = m_new;
             }
             const float neg = m_used == -INFINITY ? 0.f : -m_used;
-            float l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+            // x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU for 3 of every 4 pairs and
+            // on the FMA pipe (polynomial) for the 4th, row sum with FADD2, pack to bf16x2.
+            float la0 = 0.f, la1 = 0.f, lb0 = 0.f, lb1 = 0.f;
+            uint32_t pk[64];
 #pragma unroll
-            for (int c = 0; c < 128; c += 4) {
-                s[c] = ptx::ex2(fmaf(s[c], sl2, neg));
-                s[c + 1] = ptx::ex2(fmaf(s[c + 1], sl2, neg));
-                s[c + 2] = ptx::ex2(fmaf(s[c + 2], sl2, neg));
-                s[c + 3] = ptx::ex2(fmaf(s[c + 3], sl2, neg));
-                l0 += s[c];
-                l1 += s[c + 1];
-                l2 += s[c + 2];
-                l3 += s[c + 3];
+            for (int pi = 0; pi < 64; ++pi) {
+                float x0, x1, y0, y1;
+                ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
+                if ((pi & 3) == 3) {
+                    ptx::ex2_poly2(y0, y1, x0, x1);
+                } else {
+                    y0 = ptx::ex2(x0);
+                    y1 = ptx::ex2(x1);
+                }
+                if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
+                else ptx::fadd2(la0, la1, la0, la1, y0, y1);
+                pk[pi] = ptx::pack_bf16x2(y0, y1);
             }
-            l_run += (l0 + l1) + (l2 + l3);
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t pk[32];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) pk[e] = ptx::pack_bf16x2(s[c * 64 + 2 * e], s[c * 64 + 2 * e + 1]);
-                ptx::tmem_st32(tS + c * 32, pk);
-            }
+            l_run += (la0 + la1) + (lb0 + lb1);
+            ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
+            ptx::tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pk[32]));
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar_p);

@@ -150,6 +150,47 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// three-input max (FMNMX3, sm_100+)
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// packed fp32x2 FMA / ADD (FFMA2 / FADD2, sm_100+): (d0,d1) = (a0*b0+c0, a1*b1+c1)
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0,
+                                      float c1) {
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+// 2^x for a pair on the FMA/ALU pipes (offloads the MUFU unit): round-to-nearest
+// split x = n + f, f in [-0.5, 0.5], degree-3 minimax polynomial for 2^f (max rel.
+// error 7.5e-5, far below bf16's 2^-9), exponent added as n << 23.  x is clamped to
+// >= -126 so the result stays a (tiny) positive float; the caller keeps x <= 8.
+__device__ __forceinline__ void ex2_poly2(float& y0, float& y1, float x0, float x1) {
+    const float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic holds round(x) in the low bits
+    x0 = fmaxf(x0, -126.0f);
+    x1 = fmaxf(x1, -126.0f);
+    float t0, t1, r0, r1, f0, f1, q0, q1;
+    fadd2(t0, t1, x0, x1, kMagic, kMagic);
+    fadd2(r0, r1, t0, t1, -kMagic, -kMagic);
+    fadd2(f0, f1, x0, x1, -r0, -r1);
+    ffma2(q0, q1, f0, f1, 0.055170836f, 0.055170836f, 0.24260935f, 0.24260935f);
+    ffma2(q0, q1, q0, q1, f0, f1, 0.69326096f, 0.69326096f);
+    ffma2(q0, q1, q0, q1, f0, f1, 0.99992818f, 0.99992818f);
+    y0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+    y1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
