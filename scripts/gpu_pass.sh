@@ -15,6 +15,12 @@ if [[ $WHAT == bench || $WHAT == all ]]; then
     timeout 600 python bench.py --workload $wl --steps 20 --warmup 5 > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err; echo "bench $wl rc=$?"; cut -c1-600 $OUT/bench_$wl.json
   done
 fi
+if [[ $WHAT == ncuattn ]]; then
+  for wl in $WLS; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:gna_attn -s 3 -c 1 -o $OUT/attn_$wl \
+      python bench.py --workload $wl --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_full_$wl.log 2>&1; echo "ncu full $wl rc=$?"
+  done
+fi
 if [[ $WHAT == ncu || $WHAT == all ]]; then
   for wl in $WLS; do
     timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches_$wl.csv \
