@@ -53,27 +53,25 @@ struct Cfg {
     static constexpr int THREADS = 384;
 };
 
-struct StageBoxes {
-    int k[2][3];   // box coordinates (class-local box units) of the stage's boxes
-    int dead[2];   // 1 = filler box (odd count), masked entirely
-    int lin[2];    // linear box index inside the class box grid
-};
-
-__device__ __forceinline__ void decode_stage(const Geometry& g, const int lo[3], const int ext[3], int nkv,
-                                             int j, int kpb, StageBoxes& sb) {
-    for (int u = 0; u < kpb; ++u) {
-        int jb = j * kpb + u;
-        sb.dead[u] = jb >= nkv;
-        if (jb >= nkv) jb = 0;
-        const int k2 = jb % ext[2];
-        const int k1 = (jb / ext[2]) % ext[1];
-        const int k0 = jb / (ext[2] * ext[1]);
-        sb.k[u][0] = lo[0] + k0;
-        sb.k[u][1] = lo[1] + k1;
-        sb.k[u][2] = lo[2] + k2;
-        sb.lin[u] = ((lo[0] + k0) * g.nb[1] + (lo[1] + k1)) * g.nb[2] + (lo[2] + k2);
+// Odometer over the KV boxes of the union range [lo, hi) (row-major, last axis
+// fastest): no divisions in the mainloop.
+struct BoxIter {
+    int k[3];
+    __device__ __forceinline__ void init(const int lo[3]) {
+        k[0] = lo[0];
+        k[1] = lo[1];
+        k[2] = lo[2];
     }
-}
+    __device__ __forceinline__ void next(const int lo[3], const int hi[3]) {
+        if (++k[2] == hi[2]) {
+            k[2] = lo[2];
+            if (++k[1] == hi[1]) {
+                k[1] = lo[1];
+                ++k[0];
+            }
+        }
+    }
+};
 
 // ---- separable GNA mask of one row over one box, as a bit mask over the
 // box's rows (row-major (i0, i1, i2)).  Axis intervals [lo, hi) are relative
@@ -216,19 +214,30 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             int it = 0;
-            StageBoxes sb;
+            BoxIter bi;
+            bi.init(lo);
+            const int first_row = static_cast<int>(cls_row0 + static_cast<long long>((lo[0] * g.nb[1] + lo[1]) * g.nb[2] + lo[2]) * BV);
             for (int j = 0; j < nst; ++j) {
-                decode_stage(g, lo, ext, nkv, j, KPB, sb);
+                int rows[KPB];
+#pragma unroll
+                for (int u = 0; u < KPB; ++u) {
+                    // filler box of an odd count: reload the first box (masked by the softmax)
+                    rows[u] = (j * KPB + u < nkv)
+                                  ? static_cast<int>(cls_row0 + static_cast<long long>((bi.k[0] * g.nb[1] + bi.k[1]) * g.nb[2] + bi.k[2]) * BV)
+                                  : first_row;
+                    if (j * KPB + u < nkv) bi.next(lo, hi);
+                }
                 for (int kind = 0; kind < 2; ++kind, ++it) {
                     const int slot = it % C::NS;
                     ptx::mbar_wait(bar_kv_empty(slot), ((it / C::NS) & 1) ^ 1);
                     ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE_BYTES);
                     const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
+#pragma unroll
                     for (int u = 0; u < KPB; ++u) {
-                        const int row = static_cast<int>(cls_row0 + static_cast<long long>(sb.lin[u]) * BV);
+#pragma unroll
                         for (int h = 0; h < C::NH; ++h)
                             ptx::tma_load_2d(sKV + slot * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, tm,
-                                             bar_kv_full(slot), h * 64, row);
+                                             bar_kv_full(slot), h * 64, rows[u]);
                     }
                 }
             }
@@ -345,27 +354,42 @@ __global__ void __launch_bounds__(384, 1)
             cls_row0 + static_cast<long long>((bx[0] * g.nb[1] + bx[1]) * g.nb[2] + bx[2]) * BV + inner;
 
         const BoxMaskConsts mconst = box_mask_consts(g);
+        // Uniform (per sub-tile) coverage bits per axis over the union range: bit
+        // (k - lo[a]) set iff every in-bounds query of the sub-tile attends every key
+        // of box k on axis a (and the box is inside the class extent).  A stage needs
+        // no mask iff all its boxes are covered on all three axes.
+        uint64_t fullbits[3];
+        {
+            const bool fits = ext[0] <= 64 && ext[1] <= 64 && ext[2] <= 64;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int Lc = class_extent(g.ax[a], cc[a]);
+                const int x0 = sc[a] * g.QB[a] * g.B[a], x1 = x0 + g.QB[a] * g.B[a];
+                uint64_t bits = 0;
+                if (fits)
+                    for (int k = lo[a]; k < hi[a]; ++k)
+                        if (box_full(g.ax[a], Lc, x0, x1, k, g.B[a])) bits |= 1ull << (k - lo[a]);
+                fullbits[a] = bits;
+            }
+        }
         const float sl2 = p.scale_log2;
         float m_used = -INFINITY;
         float l_run = 0.f;
-        StageBoxes sb;
+        BoxIter bi;
+        bi.init(lo);
         for (int j = 0; j < nst; ++j) {
-            decode_stage(g, lo, ext, nkv, j, KPB, sb);
-            // per-row coverage of every key of the stage; padded rows never mask
-            bool row_full = true;
-            int rlo[KPB][3], rhi[KPB][3];
+            int kb[KPB][3];
+            bool stage_full = true;
 #pragma unroll
             for (int u = 0; u < KPB; ++u) {
+                const bool live = j * KPB + u < nkv;
 #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const int base = sb.k[u][a] * g.B[a];
-                    rlo[u][a] = wst[a] - base;
-                    rhi[u][a] = sb.dead[u] ? -1 : wen[a] - base;
-                    row_full = row_full && rlo[u][a] <= 0 && rhi[u][a] >= g.B[a];
-                }
+                for (int a = 0; a < 3; ++a) kb[u][a] = bi.k[a];
+                stage_full = stage_full && live && ((fullbits[0] >> (bi.k[0] - lo[0])) & (fullbits[1] >> (bi.k[1] - lo[1])) &
+                                                    (fullbits[2] >> (bi.k[2] - lo[2])) & 1ull);
+                if (live) bi.next(lo, hi);
+                else kb[u][0] = -(1 << 20);  // filler: no key of it is ever inside a window
             }
-            const bool warp_full = __all_sync(0xffffffffu, row_full || !valid);
-
             ptx::mbar_wait(bar_s, j & 1);
             ptx::tc_fence_after();
             float s[128];
@@ -377,10 +401,23 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
             }
-            if (!warp_full) {
+            if (!stage_full) {
                 // 128-bit row mask of the stage (1 or 2 boxes), then one select per element
-                u128 m = box_row_mask(g, mconst, rlo[0], rhi[0]);
-                if (KPB == 2) m |= box_row_mask(g, mconst, rlo[KPB - 1], rhi[KPB - 1]) << 64;
+                int rlo[3], rhi[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    rlo[a] = wst[a] - kb[0][a] * g.B[a];
+                    rhi[a] = wen[a] - kb[0][a] * g.B[a];
+                }
+                u128 m = box_row_mask(g, mconst, rlo, rhi);
+                if (KPB == 2) {
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        rlo[a] = wst[a] - kb[KPB - 1][a] * g.B[a];
+                        rhi[a] = wen[a] - kb[KPB - 1][a] * g.B[a];
+                    }
+                    m |= box_row_mask(g, mconst, rlo, rhi) << 64;
+                }
                 const uint32_t mw[4] = {static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32),
                                         static_cast<uint32_t>(m >> 64), static_cast<uint32_t>(m >> 96)};
 #pragma unroll
@@ -417,24 +454,27 @@ __global__ void __launch_bounds__(384, 1)
             // x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU for 3 of every 4 pairs and
             // on the FMA pipe (polynomial) for the 4th, row sum with FADD2, pack to bf16x2.
             float la0 = 0.f, la1 = 0.f, lb0 = 0.f, lb1 = 0.f;
-            uint32_t pk[64];
 #pragma unroll
-            for (int pi = 0; pi < 64; ++pi) {
-                float x0, x1, y0, y1;
-                ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
-                if ((pi & 3) == 3) {
-                    ptx::ex2_poly2(y0, y1, x0, x1);
-                } else {
-                    y0 = ptx::ex2(x0);
-                    y1 = ptx::ex2(x1);
+            for (int ch = 0; ch < 4; ++ch) {  // 32 columns -> 16 packed bf16x2 TMEM columns per chunk
+                uint32_t pk[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int pi = ch * 16 + q;
+                    float x0, x1, y0, y1;
+                    ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
+                    if ((pi & 3) == 3) {
+                        ptx::ex2_poly2(y0, y1, x0, x1);
+                    } else {
+                        y0 = ptx::ex2(x0);
+                        y1 = ptx::ex2(x1);
+                    }
+                    if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
+                    else ptx::fadd2(la0, la1, la0, la1, y0, y1);
+                    pk[q] = ptx::pack_bf16x2(y0, y1);
                 }
-                if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
-                else ptx::fadd2(la0, la1, la0, la1, y0, y1);
-                pk[pi] = ptx::pack_bf16x2(y0, y1);
+                ptx::tmem_st16(tS + ch * 16, pk);
             }
             l_run += (la0 + la1) + (lb0 + lb1);
-            ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
-            ptx::tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pk[32]));
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar_p);
