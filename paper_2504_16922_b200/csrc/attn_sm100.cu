@@ -35,6 +35,23 @@
 #include "kernels.h"
 #include "ptx.cuh"
 
+// Optional cycle tracing of the pipeline (build with -DGNA_TRACE, see
+// scripts/trace_attn.py): per CTA < 4, per stage, clock64() at pipeline events.
+#ifdef GNA_TRACE
+#define GNA_TRACE_CTAS 4
+#define GNA_TRACE_STAGES 256
+__device__ unsigned long long g_gna_trace[GNA_TRACE_CTAS][GNA_TRACE_STAGES][16];
+#define GT(j, ev)                                                                      \
+    do {                                                                               \
+        if (blockIdx.x < GNA_TRACE_CTAS && (j) < GNA_TRACE_STAGES)                     \
+            g_gna_trace[blockIdx.x][(j)][(ev)] = clock64();                           \
+    } while (0)
+#else
+#define GT(j, ev) \
+    do {          \
+    } while (0)
+#endif
+
 namespace gna {
 
 namespace {
@@ -168,6 +185,7 @@ __global__ void __launch_bounds__(384, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 8 * (1 + 2 * C::NS) + 40);
 
     if (threadIdx.x == 0) {
+        GT(0, 15);
         ptx::mbar_init(bar_q, 1);
         for (int s = 0; s < C::NS; ++s) {
             ptx::mbar_init(bar_kv_full(s), 1);
@@ -230,6 +248,7 @@ __global__ void __launch_bounds__(384, 1)
                 for (int kind = 0; kind < 2; ++kind, ++it) {
                     const int slot = it % C::NS;
                     ptx::mbar_wait(bar_kv_empty(slot), ((it / C::NS) & 1) ^ 1);
+                    GT(j, 12 + kind);
                     ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE_BYTES);
                     const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
 #pragma unroll
@@ -284,14 +303,17 @@ __global__ void __launch_bounds__(384, 1)
             for (int j = 0; j < nst; ++j) {
                 const int slotV = it % C::NS;
                 ptx::mbar_wait(bar_kv_full(slotV), (it / C::NS) & 1);
+                GT(j, 8);
                 ++it;
                 const bool has_next = j + 1 < nst;
                 ptx::mbar_wait(bar_p_full0, j & 1);
+                GT(j, 9);
                 ptx::tc_fence_after();
                 issue_pv(0, slotV, j > 0);
                 if (has_next) {
                     slotK = it % C::NS;
                     ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
+                    GT(j, 11);
                     ++it;
                     ptx::tc_fence_after();
                     issue_qk(0, slotK);
@@ -299,6 +321,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 if (hasB) {
                     ptx::mbar_wait(bar_p_full0 + 8, j & 1);
+                    GT(j, 10);
                     ptx::tc_fence_after();
                     issue_pv(1, slotV, j > 0);
                 }
@@ -391,16 +414,15 @@ __global__ void __launch_bounds__(384, 1)
                 else kb[u][0] = -(1 << 20);  // filler: no key of it is ever inside a window
             }
             ptx::mbar_wait(bar_s, j & 1);
+            if (r == 0) GT(j, 4 * i + 0);
             ptx::tc_fence_after();
             float s[128];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t rr[32];
-                ptx::tmem_ld32(tS + c * 32, rr);
-                ptx::tmem_wait_ld();
+            for (int c = 0; c < 4; ++c) ptx::tmem_ld32f(tS + c * 32, &s[c * 32]);
+            ptx::tmem_wait_ld();
 #pragma unroll
-                for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
-            }
+            for (int c = 0; c < 4; ++c) ptx::reg_fence32(&s[c * 32]);
+            if (r == 0) GT(j, 4 * i + 1);
             if (!stage_full) {
                 // 128-bit row mask of the stage (1 or 2 boxes), then one select per element
                 int rlo[3], rhi[3];
@@ -433,6 +455,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             const float m_tile = ptx::max3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
             const float m_new = fmaxf(m_used, m_tile);
+            if (r == 0) GT(j, 4 * i + 2);
             const bool need = m_new > m_used + 8.0f;
             if (j > 0 && __any_sync(0xffffffffu, need)) {
                 const float f = need ? ptx::ex2(m_used - m_new) : 1.0f;
@@ -476,6 +499,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             l_run += (la0 + la1) + (lb0 + lb1);
             ptx::tmem_wait_st();
+            if (r == 0) GT(j, 4 * i + 3);
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar_p);
         }
@@ -543,3 +567,14 @@ cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const C
 }
 
 }  // namespace gna
+
+#ifdef GNA_TRACE
+extern "C" int gna_debug_trace(void* host, size_t bytes) {
+    if (bytes > sizeof(g_gna_trace)) bytes = sizeof(g_gna_trace);
+    return cudaMemcpyFromSymbol(host, g_gna_trace, bytes) == cudaSuccess ? 0 : 3;
+}
+extern "C" int gna_debug_trace_reset(void) {
+    static unsigned long long zeros[GNA_TRACE_CTAS * GNA_TRACE_STAGES * 16];
+    return cudaMemcpyToSymbol(g_gna_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 3;
+}
+#endif

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgna_b200.so")
+LIB_PATH = os.environ.get("GNA_LIB_PATH") or os.path.join(_HERE, "libgna_b200.so")
 
 GNA_OK, GNA_EINVAL, GNA_EUNSUPPORTED, GNA_ECUDA, GNA_ENOMEM = range(5)
 GNA_DTYPE_BF16 = 0
