@@ -5,7 +5,8 @@ Prints per-stage event times (clock64 cycles, relative to CTA start) for CTA 0."
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2504_16922_b200 import build
-os.environ["GNA_LIB_PATH"] = build.build(trace=True)
+import paper_2504_16922_b200.gna as G
+G.LIB_PATH = build.build(trace=True)
 import numpy as np, torch
 import paper_2504_16922_b200 as gna
 from gna_inputs import WORKLOADS, make_qkv
