@@ -61,11 +61,12 @@ struct Cfg {
     static constexpr int NH = DP / 64;               // 128-byte column chunks ("halves")
     static constexpr int CHUNK_BYTES = 128 * 128;    // 128 rows x 128 B, one SW128 chunk
     static constexpr int TILE_BYTES = NH * CHUNK_BYTES;  // 128 rows x DP bf16
-    static constexpr int NS = DP == 128 ? 4 : 8;     // KV ring slots (K and V share it)
+    static constexpr int NS = DP == 128 ? 5 : 12;    // KV ring slots (K and V share it)
     static constexpr int KPB = 128 / BV;             // boxes per 128-row tile
     static constexpr int Q_OFF = 0;
     static constexpr int KV_OFF = 2 * TILE_BYTES;
     static constexpr int BAR_OFF = KV_OFF + NS * TILE_BYTES;
+    static constexpr int PF = 3;                      // stages prefetched into L2 ahead of the ring
     static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
     static constexpr int THREADS = 384;
 };
@@ -232,17 +233,32 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             int it = 0;
-            BoxIter bi;
+            BoxIter bi, bp;  // load cursor and L2-prefetch cursor (C::PF stages ahead)
             bi.init(lo);
+            bp.init(lo);
             const int first_row = static_cast<int>(cls_row0 + static_cast<long long>((lo[0] * g.nb[1] + lo[1]) * g.nb[2] + lo[2]) * BV);
+            auto box_row = [&](const BoxIter& b) {
+                return static_cast<int>(cls_row0 + static_cast<long long>((b.k[0] * g.nb[1] + b.k[1]) * g.nb[2] + b.k[2]) * BV);
+            };
+            int npf = 0;  // boxes prefetched so far
+            auto prefetch_upto = [&](int nbox) {
+                for (; npf < nbox && npf < nkv; ++npf) {
+                    const int row = box_row(bp);
+#pragma unroll
+                    for (int h = 0; h < C::NH; ++h) {
+                        ptx::tma_prefetch_2d(&tmap_k, h * 64, row);
+                        ptx::tma_prefetch_2d(&tmap_v, h * 64, row);
+                    }
+                    bp.next(lo, hi);
+                }
+            };
+            prefetch_upto(C::PF * KPB);
             for (int j = 0; j < nst; ++j) {
                 int rows[KPB];
 #pragma unroll
                 for (int u = 0; u < KPB; ++u) {
                     // filler box of an odd count: reload the first box (masked by the softmax)
-                    rows[u] = (j * KPB + u < nkv)
-                                  ? static_cast<int>(cls_row0 + static_cast<long long>((bi.k[0] * g.nb[1] + bi.k[1]) * g.nb[2] + bi.k[2]) * BV)
-                                  : first_row;
+                    rows[u] = (j * KPB + u < nkv) ? box_row(bi) : first_row;
                     if (j * KPB + u < nkv) bi.next(lo, hi);
                 }
                 for (int kind = 0; kind < 2; ++kind, ++it) {
@@ -259,6 +275,7 @@ __global__ void __launch_bounds__(384, 1)
                                              bar_kv_full(slot), h * 64, rows[u]);
                     }
                 }
+                prefetch_upto((j + 1 + C::PF) * KPB);
             }
         }
     } else if (warp == 9) {
@@ -445,15 +462,16 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int c = 0; c < 128; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
             }
-            float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+            float mx[8];
 #pragma unroll
-            for (int c = 4; c < 128; c += 8) {
-                mx0 = ptx::max3(mx0, s[c], s[c + 1]);
-                mx1 = ptx::max3(mx1, s[c + 2], s[c + 3]);
-                mx2 = ptx::max3(mx2, s[c + 4], s[c + 5]);
-                mx3 = ptx::max3(mx3, s[c + 6], s[c + 7]);
+            for (int e = 0; e < 8; ++e) mx[e] = s[e];
+#pragma unroll
+            for (int c = 8; c < 128; c += 16) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) mx[e] = ptx::max3(mx[e], s[c + 2 * e], s[c + 2 * e + 1]);
             }
-            const float m_tile = ptx::max3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
+            const float m_tile =
+                ptx::max3(ptx::max3(mx[0], mx[1], mx[2]), ptx::max3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
             const float m_new = fmaxf(m_used, m_tile);
             if (r == 0) GT(j, 4 * i + 2);
             const bool need = m_new > m_used + 8.0f;
@@ -485,7 +503,7 @@ __global__ void __launch_bounds__(384, 1)
                     const int pi = ch * 16 + q;
                     float x0, x1, y0, y1;
                     ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
-                    if ((pi & 3) == 3) {
+                    if ((pi & 1) == 1) {
                         ptx::ex2_poly2(y0, y1, x0, x1);
                     } else {
                         y0 = ptx::ex2(x0);

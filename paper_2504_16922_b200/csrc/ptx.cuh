@@ -49,6 +49,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* desc, uint
         : "memory");
 }
 
+// 2-D tile prefetch into L2 (no smem, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_2d(const void* desc, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(desc)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem),
