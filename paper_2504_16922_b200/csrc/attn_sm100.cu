@@ -492,30 +492,45 @@ __global__ void __launch_bounds__(384, 1)
                 m_used = m_new;
             }
             const float neg = m_used == -INFINITY ? 0.f : -m_used;
-            // x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU for 3 of every 4 pairs and
-            // on the FMA pipe (polynomial) for the 4th, row sum with FADD2, pack to bf16x2.
-            float la0 = 0.f, la1 = 0.f, lb0 = 0.f, lb1 = 0.f;
+            // In separate, fully unrolled phases so the MUFU stream is back to back:
+            // x = s * scale*log2(e) - m (FFMA2); 2^x on MUFU for even pairs and on the
+            // FMA pipe (polynomial) for odd pairs; row sum with 8 FADD2 chains; bf16x2
+            // pack and TMEM store in four 16-column chunks.
+#pragma unroll
+            for (int pi = 0; pi < 64; ++pi)
+                ptx::ffma2(s[2 * pi], s[2 * pi + 1], s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
+#pragma unroll
+            for (int pi = 0; pi < 64; pi += 2) {
+                s[2 * pi] = ptx::ex2(s[2 * pi]);
+                s[2 * pi + 1] = ptx::ex2(s[2 * pi + 1]);
+                ptx::ex2_poly2(s[2 * pi + 2], s[2 * pi + 3], s[2 * pi + 2], s[2 * pi + 3]);
+            }
+            {
+                float la[8], lb[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    la[e] = s[2 * e];
+                    lb[e] = s[2 * e + 1];
+                }
+#pragma unroll
+                for (int pi = 8; pi < 64; pi += 8) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        ptx::fadd2(la[e], lb[e], la[e], lb[e], s[2 * (pi + e)], s[2 * (pi + e) + 1]);
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) ptx::fadd2(la[e], lb[e], la[e], lb[e], la[e + 4], lb[e + 4]);
+                ptx::fadd2(la[0], lb[0], la[0], lb[0], la[2], lb[2]);
+                ptx::fadd2(la[1], lb[1], la[1], lb[1], la[3], lb[3]);
+                l_run += (la[0] + lb[0]) + (la[1] + lb[1]);
+            }
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) {  // 32 columns -> 16 packed bf16x2 TMEM columns per chunk
                 uint32_t pk[16];
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const int pi = ch * 16 + q;
-                    float x0, x1, y0, y1;
-                    ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
-                    if ((pi & 1) == 1) {
-                        ptx::ex2_poly2(y0, y1, x0, x1);
-                    } else {
-                        y0 = ptx::ex2(x0);
-                        y1 = ptx::ex2(x1);
-                    }
-                    if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
-                    else ptx::fadd2(la0, la1, la0, la1, y0, y1);
-                    pk[q] = ptx::pack_bf16x2(y0, y1);
-                }
+                for (int q = 0; q < 16; ++q) pk[q] = ptx::pack_bf16x2(s[ch * 32 + 2 * q], s[ch * 32 + 2 * q + 1]);
                 ptx::tmem_st16(tS + ch * 16, pk);
             }
-            l_run += (la0 + la1) + (lb0 + lb1);
             ptx::tmem_wait_st();
             if (r == 0) GT(j, 4 * i + 3);
             ptx::tc_fence_before();
