@@ -493,17 +493,20 @@ __global__ void __launch_bounds__(384, 1)
             }
             const float neg = m_used == -INFINITY ? 0.f : -m_used;
             // In separate, fully unrolled phases so the MUFU stream is back to back:
-            // x = s * scale*log2(e) - m (FFMA2); 2^x on MUFU for even pairs and on the
-            // FMA pipe (polynomial) for odd pairs; row sum with 8 FADD2 chains; bf16x2
+            // x = s * scale*log2(e) - m (FFMA2); 2^x on MUFU for 3 pairs in 4 and on
+            // the FMA pipe (polynomial) for the 4th; row sum with 8 FADD2 chains; bf16x2
             // pack and TMEM store in four 16-column chunks.
 #pragma unroll
             for (int pi = 0; pi < 64; ++pi)
                 ptx::ffma2(s[2 * pi], s[2 * pi + 1], s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
 #pragma unroll
-            for (int pi = 0; pi < 64; pi += 2) {
-                s[2 * pi] = ptx::ex2(s[2 * pi]);
-                s[2 * pi + 1] = ptx::ex2(s[2 * pi + 1]);
-                ptx::ex2_poly2(s[2 * pi + 2], s[2 * pi + 3], s[2 * pi + 2], s[2 * pi + 3]);
+            for (int pi = 0; pi < 64; ++pi) {
+                if ((pi & 3) == 3) {  // 1 pair in 4 on the FMA pipe (scripts/micro/exp_phase.cu: best split)
+                    ptx::ex2_poly2(s[2 * pi], s[2 * pi + 1], s[2 * pi], s[2 * pi + 1]);
+                } else {
+                    s[2 * pi] = ptx::ex2(s[2 * pi]);
+                    s[2 * pi + 1] = ptx::ex2(s[2 * pi + 1]);
+                }
             }
             {
                 float la[8], lb[8];
