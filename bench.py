@@ -110,8 +110,9 @@ def _dist():
 
 
 def _max_over_ranks(vals, ws, device):
+    """Element-wise max over ranks (device-measured times); identity at N=1."""
     if ws == 1:
-        return vals
+        return list(vals)
     import torch
     import torch.distributed as dist
 
@@ -355,6 +356,86 @@ def run_ours(args, ws, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_split(args, ws, rank, local):
+    """--mode split: Q-tile splitting of ONE problem (strong scaling).  Every rank
+    holds the full (replicated) inputs, permutes them, and runs the attention on
+    its contiguous share of the global work list; no collective on the data path.
+    Verification (untimed): outputs are assembled with an NCCL all_reduce(SUM)
+    over zero-initialised shards and compared bit for bit with a single launch."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_16922_b200 as gna
+    from paper_2504_16922_b200.shard import work_range
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = WORKLOADS[args.workload]
+    f = w.full()
+    B, H, D = w.batch, w.heads, w.head_dim
+    q, k, v = (t.to(dev) for t in make_qkv(B, w.spatial, H, D, seed=SEED))
+    win, st, dil, cau = f["window"], f["stride"], f["dilation"], f["causal"]
+    info = gna.plan_info(B, H, D, **f)
+    rng = work_range(info["n_work"], ws, rank)
+    wsb = torch.zeros(info["workspace_bytes"], dtype=torch.uint8, device=dev)
+    out = torch.zeros_like(q)
+    lse = torch.zeros(q.shape[:-1], dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step():
+        gna.permute(q, k, v, out, win, st, dil, cau, workspace=wsb)
+        gna.attention_permuted(q, k, v, out, win, st, dil, cau, workspace=wsb, work_range=rng)
+        gna.unpermute(q, k, v, out, lse, win, st, dil, cau, workspace=wsb)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ts = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    total_ms = _max_over_ranks([sum(ts)], ws, dev)[0]
+    # ---- verification gather (untimed): shards over a zeroed workspace, SUM-assembled
+    wsb.zero_()
+    out.zero_()
+    lse.zero_()
+    step()
+    if ws > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM)
+        dist.all_reduce(lse, op=dist.ReduceOp.SUM)
+    ok = None
+    if rank == 0:
+        ref_o, ref_l = gna.forward(q, k, v, win, st, dil, cau)
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(ref_o, out) and torch.equal(ref_l, lse))
+    if rank != 0:
+        return
+    eff_flops = 4.0 * D * info["kept_pairs"] * B * H
+    ms = total_ms / args.steps
+    peak_burst, peak_sus, hbm, peak_kind = _peaks()
+    line = {
+        "metric": METRIC, "value": eff_flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": w.name, "mode": "split (Q-tile splitting of one problem)",
+                   "work_items": info["n_work"], "l2": "flushed (256 MiB write) between timed steps"},
+        "verified_bitwise_vs_single_launch": ok, "gpu_launches": 3 * args.steps, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -364,10 +445,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="weak", choices=["weak", "split"],
+                    help="weak: each rank runs its own batch shard; split: Q-tile splitting of one problem")
     args = ap.parse_args()
     ws, rank, local = _dist()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif args.mode == "split":
+        run_split(args, ws, rank, local)
     else:
         run_ours(args, ws, rank, local)
     if ws > 1:

@@ -515,6 +515,7 @@ int do_attention(const gna_args* a, Ctx& c) {
     if (wb < 0) wb = 0;
     if (wb > we) return fail(GNA_EINVAL, "work_begin > work_end");
     p.work_begin = wb;
+    p.work_end = we;
     p.o_perm = c.ws + c.L.o;
     p.lse_perm = reinterpret_cast<float*>(c.ws + c.L.lse);
     const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));

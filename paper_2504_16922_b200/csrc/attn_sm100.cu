@@ -66,7 +66,6 @@ struct Cfg {
     static constexpr int Q_OFF = 0;
     static constexpr int KV_OFF = 2 * TILE_BYTES;
     static constexpr int BAR_OFF = KV_OFF + NS * TILE_BYTES;
-    static constexpr int PF = 3;                      // stages prefetched into L2 ahead of the ring
     static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
     static constexpr int THREADS = 384;
 };
@@ -133,6 +132,42 @@ __device__ __forceinline__ u128 box_row_mask(const Geometry& g, const BoxMaskCon
 
 }  // namespace
 
+// One work item as every role sees it (decoded independently by each warp).
+struct WorkItem {
+    long long cls_row0;  // first permuted row of this (batch*head, class)
+    int cls, subA, subB;
+    int lo[3], hi[3];    // union KV box range
+    int nkv, nst;        // boxes, 128-row stages
+};
+
+template <int KPB>
+__device__ __forceinline__ void load_item(const AttnParams& p, long long w, WorkItem& it) {
+    const Geometry& g = p.g;
+    const long long bh = w / p.n_items;
+    const int4 e = p.items[w % p.n_items];
+    it.cls = e.x;
+    it.subA = e.y;
+    it.subB = e.z;
+    sub_range(g, it.cls, it.subA, it.lo, it.hi);
+    if (it.subB >= 0) {
+        int lb[3], hb[3];
+        sub_range(g, it.cls, it.subB, lb, hb);
+        for (int a = 0; a < 3; ++a) {
+            it.lo[a] = min(it.lo[a], lb[a]);
+            it.hi[a] = max(it.hi[a], hb[a]);
+        }
+    }
+    it.nkv = (it.hi[0] - it.lo[0]) * (it.hi[1] - it.lo[1]) * (it.hi[2] - it.lo[2]);
+    it.nst = (it.nkv + KPB - 1) / KPB;
+    it.cls_row0 = ((bh * g.ncls + it.cls) * static_cast<long long>(g.nbox)) * (128 / KPB);
+}
+
+// Persistent kernel: grid = min(#work items, #SMs); CTA b processes work items
+// w = work_begin + b + k * gridDim.x (items are LPT-ordered by the planner).  The
+// roles run ahead across item boundaries: the producer loads the next item's Q as
+// soon as the last QK^T of the current item has been issued (q_empty), the MMA
+// warp starts the next item's QK^T while the softmax warps run the epilogue, and
+// the first PV of the next item waits only for the epilogue's TMEM read (o_empty).
 template <int DP, int BV>
 __global__ void __launch_bounds__(384, 1)
     gna_attn_sm100(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tmap_q,
@@ -146,57 +181,35 @@ __global__ void __launch_bounds__(384, 1)
     const Geometry& g = p.g;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-
-    // ---------------------------------------------------------- work item
-    const long long w = static_cast<long long>(blockIdx.x) + p.work_begin;
-    const long long bh = w / p.n_items;
-    const int4 item = p.items[w % p.n_items];
-    const int cls = item.x, subA = item.y, subB = item.z;
-    const bool hasB = subB >= 0;
-
-    int lo[3], hi[3];
-    sub_range(g, cls, subA, lo, hi);
-    if (hasB) {
-        int lb[3], hb[3];
-        sub_range(g, cls, subB, lb, hb);
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = min(lo[a], lb[a]);
-            hi[a] = max(hi[a], hb[a]);
-        }
-    }
-    int ext[3];
-    for (int a = 0; a < 3; ++a) ext[a] = hi[a] - lo[a];
-    const int nkv = ext[0] * ext[1] * ext[2];
-    const int nst = (nkv + KPB - 1) / KPB;
-    if (nst <= 0) return;  // uniform for the CTA: empty item
-
-    // rows of this (bh, class) start here in the permuted buffers
-    const long long cls_row0 = ((bh * g.ncls + cls) * static_cast<long long>(g.nbox)) * BV;
+    const long long w_first = p.work_begin + blockIdx.x, w_end = p.work_end, w_step = gridDim.x;
 
     // ---------------------------------------------------------- smem carve
     const uint32_t sQ = sbase + C::Q_OFF;
     const uint32_t sKV = sbase + C::KV_OFF;
     const uint32_t bar0 = sbase + C::BAR_OFF;
-    const uint32_t bar_q = bar0;
-    auto bar_kv_full = [&](int s) { return bar0 + 8u * (1 + s); };
-    auto bar_kv_empty = [&](int s) { return bar0 + 8u * (1 + C::NS + s); };
-    const uint32_t bar_s_full0 = bar0 + 8u * (1 + 2 * C::NS);
-    const uint32_t bar_p_full0 = bar_s_full0 + 16;
-    const uint32_t bar_o_full = bar_p_full0 + 16;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 8 * (1 + 2 * C::NS) + 40);
+    const uint32_t bar_q_full = bar0, bar_q_empty = bar0 + 8;
+    auto bar_kv_full = [&](int s) { return bar0 + 16u + 8u * s; };
+    auto bar_kv_empty = [&](int s) { return bar0 + 16u + 8u * (C::NS + s); };
+    const uint32_t bar_s_full0 = bar0 + 16u + 16u * C::NS;  // [2]
+    const uint32_t bar_p_full0 = bar_s_full0 + 16;           // [2]
+    const uint32_t bar_o_full0 = bar_p_full0 + 16;           // [2]
+    const uint32_t bar_o_empty0 = bar_o_full0 + 16;          // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 16 + 16 * C::NS + 64);
 
     if (threadIdx.x == 0) {
         GT(0, 15);
-        ptx::mbar_init(bar_q, 1);
+        ptx::mbar_init(bar_q_full, 1);
+        ptx::mbar_init(bar_q_empty, 1);
         for (int s = 0; s < C::NS; ++s) {
             ptx::mbar_init(bar_kv_full(s), 1);
             ptx::mbar_init(bar_kv_empty(s), 1);
         }
-        ptx::mbar_init(bar_s_full0, 1);
-        ptx::mbar_init(bar_s_full0 + 8, 1);
-        ptx::mbar_init(bar_p_full0, 128);
-        ptx::mbar_init(bar_p_full0 + 8, 128);
-        ptx::mbar_init(bar_o_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(bar_s_full0 + 8 * i, 1);
+            ptx::mbar_init(bar_p_full0 + 8 * i, 128);
+            ptx::mbar_init(bar_o_full0 + 8 * i, 1);
+            ptx::mbar_init(bar_o_empty0 + 8 * i, 128);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 8) {
@@ -216,82 +229,74 @@ __global__ void __launch_bounds__(384, 1)
             ptx::tma_prefetch_desc(&tmap_q);
             ptx::tma_prefetch_desc(&tmap_k);
             ptx::tma_prefetch_desc(&tmap_v);
-            ptx::mbar_expect_tx(bar_q, (hasB ? 2 : 1) * C::TILE_BYTES);
-            for (int i = 0; i < (hasB ? 2 : 1); ++i) {
-                const int sub = i == 0 ? subA : subB;
-                int sc[3];
-                sub_coords(g, sub, sc);
-                for (int u = 0; u < KPB; ++u) {
-                    // box u of the sub-tile, row-major over the sub-tile's QB box block
-                    const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
-                    const int blin = ((sc[0] * g.QB[0] + u0) * g.nb[1] + (sc[1] * g.QB[1] + u1)) * g.nb[2] +
-                                     (sc[2] * g.QB[2] + u2);
-                    const int row = static_cast<int>(cls_row0 + static_cast<long long>(blin) * BV);
-                    for (int h = 0; h < C::NH; ++h)
-                        ptx::tma_load_2d(sQ + i * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, &tmap_q,
-                                         bar_q, h * 64, row);
-                }
-            }
-            int it = 0;
-            BoxIter bi, bp;  // load cursor and L2-prefetch cursor (C::PF stages ahead)
-            bi.init(lo);
-            bp.init(lo);
-            const int first_row = static_cast<int>(cls_row0 + static_cast<long long>((lo[0] * g.nb[1] + lo[1]) * g.nb[2] + lo[2]) * BV);
-            auto box_row = [&](const BoxIter& b) {
-                return static_cast<int>(cls_row0 + static_cast<long long>((b.k[0] * g.nb[1] + b.k[1]) * g.nb[2] + b.k[2]) * BV);
-            };
-            int npf = 0;  // boxes prefetched so far
-            auto prefetch_upto = [&](int nbox) {
-                for (; npf < nbox && npf < nkv; ++npf) {
-                    const int row = box_row(bp);
-#pragma unroll
-                    for (int h = 0; h < C::NH; ++h) {
-                        ptx::tma_prefetch_2d(&tmap_k, h * 64, row);
-                        ptx::tma_prefetch_2d(&tmap_v, h * 64, row);
+            int it = 0, n_local = 0;
+            WorkItem wi;
+            for (long long w = w_first; w < w_end; w += w_step) {
+                load_item<KPB>(p, w, wi);
+                if (wi.nst <= 0) continue;
+                const bool hasB = wi.subB >= 0;
+                if (n_local > 0) ptx::mbar_wait(bar_q_empty, (n_local - 1) & 1);
+                ptx::mbar_expect_tx(bar_q_full, (hasB ? 2 : 1) * C::TILE_BYTES);
+                for (int i = 0; i < (hasB ? 2 : 1); ++i) {
+                    int sc[3];
+                    sub_coords(g, i == 0 ? wi.subA : wi.subB, sc);
+                    for (int u = 0; u < KPB; ++u) {
+                        // box u of the sub-tile, row-major over the sub-tile's QB box block
+                        const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
+                        const int blin = ((sc[0] * g.QB[0] + u0) * g.nb[1] + (sc[1] * g.QB[1] + u1)) * g.nb[2] +
+                                         (sc[2] * g.QB[2] + u2);
+                        const int row = static_cast<int>(wi.cls_row0 + static_cast<long long>(blin) * BV);
+                        for (int h = 0; h < C::NH; ++h)
+                            ptx::tma_load_2d(sQ + i * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, &tmap_q,
+                                             bar_q_full, h * 64, row);
                     }
-                    bp.next(lo, hi);
                 }
-            };
-            prefetch_upto(C::PF * KPB);
-            for (int j = 0; j < nst; ++j) {
-                int rows[KPB];
-#pragma unroll
-                for (int u = 0; u < KPB; ++u) {
-                    // filler box of an odd count: reload the first box (masked by the softmax)
-                    rows[u] = (j * KPB + u < nkv) ? box_row(bi) : first_row;
-                    if (j * KPB + u < nkv) bi.next(lo, hi);
-                }
-                for (int kind = 0; kind < 2; ++kind, ++it) {
-                    const int slot = it % C::NS;
-                    ptx::mbar_wait(bar_kv_empty(slot), ((it / C::NS) & 1) ^ 1);
-                    GT(j, 12 + kind);
-                    ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE_BYTES);
-                    const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
+                BoxIter bi;
+                bi.init(wi.lo);
+                auto box_row = [&](const BoxIter& b) {
+                    return static_cast<int>(wi.cls_row0 +
+                                            static_cast<long long>((b.k[0] * g.nb[1] + b.k[1]) * g.nb[2] + b.k[2]) * BV);
+                };
+                const int first_row = box_row(bi);
+                for (int j = 0; j < wi.nst; ++j) {
+                    int rows[KPB];
 #pragma unroll
                     for (int u = 0; u < KPB; ++u) {
+                        // filler box of an odd count: reload the first box (masked by the softmax)
+                        const bool live = j * KPB + u < wi.nkv;
+                        rows[u] = live ? box_row(bi) : first_row;
+                        if (live) bi.next(wi.lo, wi.hi);
+                    }
+                    for (int kind = 0; kind < 2; ++kind, ++it) {
+                        const int slot = it % C::NS;
+                        ptx::mbar_wait(bar_kv_empty(slot), ((it / C::NS) & 1) ^ 1);
+                        if (n_local == 0) GT(j, 12 + kind);
+                        ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE_BYTES);
+                        const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
 #pragma unroll
-                        for (int h = 0; h < C::NH; ++h)
-                            ptx::tma_load_2d(sKV + slot * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, tm,
-                                             bar_kv_full(slot), h * 64, rows[u]);
+                        for (int u = 0; u < KPB; ++u) {
+#pragma unroll
+                            for (int h = 0; h < C::NH; ++h)
+                                ptx::tma_load_2d(sKV + slot * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, tm,
+                                                 bar_kv_full(slot), h * 64, rows[u]);
+                        }
                     }
                 }
-                prefetch_upto((j + 1 + C::PF) * KPB);
+                ++n_local;
             }
         }
-    } else if (warp == 9) {
+      } else if (warp == 9) {
         // ======================================================= MMA issuer
         if (lane == 0) {
             constexpr uint32_t IDESC_QK = ptx::idesc_bf16(128, 128, 0, 0);
             constexpr uint32_t IDESC_PV = ptx::idesc_bf16(128, DP, 0, 1);
-            const uint32_t tS0 = tmem, tS1 = tmem + 128;
-            const uint32_t tO0 = tmem + 256, tO1 = tmem + 384;
             auto issue_qk = [&](int i, int slot) {
                 const uint32_t qa = sQ + i * C::TILE_BYTES;
                 const uint32_t kb = sKV + slot * C::TILE_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < DP / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * C::CHUNK_BYTES + (kk & 3) * 32;
-                    ptx::mma_ss(i == 0 ? tS0 : tS1, ptx::smem_desc_sw128(qa + off, 16, 1024),
+                    ptx::mma_ss(tmem + 128 * i, ptx::smem_desc_sw128(qa + off, 16, 1024),
                                 ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
                 }
             };
@@ -299,86 +304,116 @@ __global__ void __launch_bounds__(384, 1)
                 const uint32_t vb = sKV + slot * C::TILE_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    ptx::mma_ts(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + kk * 8,
+                    ptx::mma_ts(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8,
                                 ptx::smem_desc_sw128(vb + kk * 2048, C::CHUNK_BYTES, 1024), IDESC_PV,
                                 (acc || kk > 0) ? 1u : 0u);
                 }
             };
-            ptx::mbar_wait(bar_q, 0);
-            int it = 0;
-            int slotK = it % C::NS;
-            ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
-            ++it;
-            ptx::tc_fence_after();
-            issue_qk(0, slotK);
-            ptx::mma_commit(bar_s_full0);
-            if (hasB) {
-                issue_qk(1, slotK);
-                ptx::mma_commit(bar_s_full0 + 8);
-            }
-            ptx::mma_commit(bar_kv_empty(slotK));
-            for (int j = 0; j < nst; ++j) {
-                const int slotV = it % C::NS;
-                ptx::mbar_wait(bar_kv_full(slotV), (it / C::NS) & 1);
-                GT(j, 8);
+            int it = 0, n_local = 0;
+            int cnt_p[2] = {0, 0};  // P_i stages consumed
+            int n_o[2] = {0, 0};    // items whose O_i was finalised
+            WorkItem wi;
+            for (long long w = w_first; w < w_end; w += w_step) {
+                load_item<KPB>(p, w, wi);
+                if (wi.nst <= 0) continue;
+                const bool hasB = wi.subB >= 0;
+                const int nst = wi.nst;
+                ptx::mbar_wait(bar_q_full, n_local & 1);
+                int slotK = it % C::NS;
+                ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
                 ++it;
-                const bool has_next = j + 1 < nst;
-                ptx::mbar_wait(bar_p_full0, j & 1);
-                GT(j, 9);
                 ptx::tc_fence_after();
-                issue_pv(0, slotV, j > 0);
-                if (has_next) {
-                    slotK = it % C::NS;
-                    ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
-                    GT(j, 11);
-                    ++it;
-                    ptx::tc_fence_after();
-                    issue_qk(0, slotK);
-                    ptx::mma_commit(bar_s_full0);
-                }
+                issue_qk(0, slotK);
+                ptx::mma_commit(bar_s_full0);
                 if (hasB) {
-                    ptx::mbar_wait(bar_p_full0 + 8, j & 1);
-                    GT(j, 10);
+                    issue_qk(1, slotK);
+                    ptx::mma_commit(bar_s_full0 + 8);
+                }
+                if (nst == 1) ptx::mma_commit(bar_q_empty);  // last QK^T of the item issued
+                ptx::mma_commit(bar_kv_empty(slotK));
+                for (int j = 0; j < nst; ++j) {
+                    const int slotV = it % C::NS;
+                    ptx::mbar_wait(bar_kv_full(slotV), (it / C::NS) & 1);
+                    if (n_local == 0) GT(j, 8);
+                    ++it;
+                    const bool has_next = j + 1 < nst;
+                    ptx::mbar_wait(bar_p_full0, cnt_p[0] & 1);
+                    ++cnt_p[0];
+                    if (j == 0 && n_o[0] > 0) ptx::mbar_wait(bar_o_empty0, (n_o[0] - 1) & 1);
+                    if (n_local == 0) GT(j, 9);
                     ptx::tc_fence_after();
-                    issue_pv(1, slotV, j > 0);
-                }
-                ptx::mma_commit(bar_kv_empty(slotV));
-                if (has_next) {
-                    if (hasB) {
-                        issue_qk(1, slotK);
-                        ptx::mma_commit(bar_s_full0 + 8);
+                    issue_pv(0, slotV, j > 0);
+                    if (has_next) {
+                        slotK = it % C::NS;
+                        ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
+                        if (n_local == 0) GT(j, 11);
+                        ++it;
+                        ptx::tc_fence_after();
+                        issue_qk(0, slotK);
+                        ptx::mma_commit(bar_s_full0);
                     }
-                    ptx::mma_commit(bar_kv_empty(slotK));
+                    if (hasB) {
+                        ptx::mbar_wait(bar_p_full0 + 8, cnt_p[1] & 1);
+                        ++cnt_p[1];
+                        if (j == 0 && n_o[1] > 0) ptx::mbar_wait(bar_o_empty0 + 8, (n_o[1] - 1) & 1);
+                        if (n_local == 0) GT(j, 10);
+                        ptx::tc_fence_after();
+                        issue_pv(1, slotV, j > 0);
+                    }
+                    ptx::mma_commit(bar_kv_empty(slotV));
+                    if (has_next) {
+                        if (hasB) {
+                            issue_qk(1, slotK);
+                            ptx::mma_commit(bar_s_full0 + 8);
+                        }
+                        if (j + 2 == nst) ptx::mma_commit(bar_q_empty);  // last QK^T of the item issued
+                        ptx::mma_commit(bar_kv_empty(slotK));
+                    }
                 }
+                ptx::mma_commit(bar_o_full0);
+                ++n_o[0];
+                if (hasB) {
+                    ptx::mma_commit(bar_o_full0 + 8);
+                    ++n_o[1];
+                }
+                ++n_local;
             }
-            ptx::mma_commit(bar_o_full);
         }
       }
     } else {
       asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
-      if (warp < 4 || hasB) {
-        // ==================================================== softmax WG i
-        const int i = warp >> 2;
-        const int wl = warp & 3;
-        const int r = threadIdx.x & 127;  // row of the sub-tile == TMEM lane
-        const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
-        const uint32_t tS = tmem + i * 128 + lane_off;
-        const uint32_t tO = tmem + 256 + i * 128 + lane_off;
-        const uint32_t bar_s = bar_s_full0 + 8 * i;
-        const uint32_t bar_p = bar_p_full0 + 8 * i;
-        const int sub = i == 0 ? subA : subB;
+      // ==================================================== softmax WG i
+      const int i = warp >> 2;
+      const int wl = warp & 3;
+      const int r = threadIdx.x & 127;  // row of the sub-tile == TMEM lane
+      const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
+      const uint32_t tS = tmem + i * 128 + lane_off;
+      const uint32_t tO = tmem + 256 + i * 128 + lane_off;
+      const uint32_t bar_s = bar_s_full0 + 8 * i;
+      const uint32_t bar_p = bar_p_full0 + 8 * i;
+      const BoxMaskConsts mconst = box_mask_consts(g);
+      const float sl2 = p.scale_log2;
+      int cnt_s = 0, n_done = 0, n_local = 0;
+      WorkItem wi;
+      for (long long w = w_first; w < w_end; w += w_step) {
+        load_item<KPB>(p, w, wi);
+        if (wi.nst <= 0) continue;
+        ++n_local;
+        const int sub = i == 0 ? wi.subA : wi.subB;
+        if (sub < 0) continue;
+        const int nst = wi.nst, nkv = wi.nkv;
+        const int* lo = wi.lo;
+        const int* hi = wi.hi;
 
         // ---- this row's token and its per-axis window (class-local)
         int cc[3], sc[3];
-        class_coords(g, cls, cc);
+        class_coords(g, wi.cls, cc);
         sub_coords(g, sub, sc);
         const int ub = r / BV, inner = r % BV;
         const int u2 = ub % g.QB[2], u1 = (ub / g.QB[2]) % g.QB[1], u0 = ub / (g.QB[2] * g.QB[1]);
         const int bx[3] = {sc[0] * g.QB[0] + u0, sc[1] * g.QB[1] + u1, sc[2] * g.QB[2] + u2};
-        const int in2 = inner & (g.B[2] - 1);
-        const int in1 = (inner >> g.logB[2]) & (g.B[1] - 1);
-        const int in0 = inner >> (g.logB[2] + g.logB[1]);
-        const int xin[3] = {in0, in1, in2};
+        const int xin[3] = {inner >> (g.logB[2] + g.logB[1]), (inner >> g.logB[2]) & (g.B[1] - 1),
+                            inner & (g.B[2] - 1)};
         int wst[3], wen[3];
         bool valid = true;
         for (int a = 0; a < 3; ++a) {
@@ -391,16 +426,15 @@ __global__ void __launch_bounds__(384, 1)
             window(g.ax[a], Lc, x, &wst[a], &wen[a]);
         }
         const long long row_g =
-            cls_row0 + static_cast<long long>((bx[0] * g.nb[1] + bx[1]) * g.nb[2] + bx[2]) * BV + inner;
+            wi.cls_row0 + static_cast<long long>((bx[0] * g.nb[1] + bx[1]) * g.nb[2] + bx[2]) * BV + inner;
 
-        const BoxMaskConsts mconst = box_mask_consts(g);
         // Uniform (per sub-tile) coverage bits per axis over the union range: bit
         // (k - lo[a]) set iff every in-bounds query of the sub-tile attends every key
         // of box k on axis a (and the box is inside the class extent).  A stage needs
         // no mask iff all its boxes are covered on all three axes.
         uint64_t fullbits[3];
         {
-            const bool fits = ext[0] <= 64 && ext[1] <= 64 && ext[2] <= 64;
+            const bool fits = hi[0] - lo[0] <= 64 && hi[1] - lo[1] <= 64 && hi[2] - lo[2] <= 64;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int Lc = class_extent(g.ax[a], cc[a]);
@@ -412,7 +446,6 @@ __global__ void __launch_bounds__(384, 1)
                 fullbits[a] = bits;
             }
         }
-        const float sl2 = p.scale_log2;
         float m_used = -INFINITY;
         float l_run = 0.f;
         BoxIter bi;
@@ -430,8 +463,10 @@ __global__ void __launch_bounds__(384, 1)
                 if (live) bi.next(lo, hi);
                 else kb[u][0] = -(1 << 20);  // filler: no key of it is ever inside a window
             }
-            ptx::mbar_wait(bar_s, j & 1);
-            if (r == 0) GT(j, 4 * i + 0);
+
+            ptx::mbar_wait(bar_s, cnt_s & 1);
+            ++cnt_s;
+            if (r == 0 && n_local == 1) GT(j, 4 * i + 0);
             ptx::tc_fence_after();
             float s[128];
 #pragma unroll
@@ -439,7 +474,7 @@ __global__ void __launch_bounds__(384, 1)
             ptx::tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 4; ++c) ptx::reg_fence32(&s[c * 32]);
-            if (r == 0) GT(j, 4 * i + 1);
+            if (r == 0 && n_local == 1) GT(j, 4 * i + 1);
             if (!stage_full) {
                 // 128-bit row mask of the stage (1 or 2 boxes), then one select per element
                 int rlo[3], rhi[3];
@@ -473,7 +508,7 @@ __global__ void __launch_bounds__(384, 1)
             const float m_tile =
                 ptx::max3(ptx::max3(mx[0], mx[1], mx[2]), ptx::max3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
             const float m_new = fmaxf(m_used, m_tile);
-            if (r == 0) GT(j, 4 * i + 2);
+            if (r == 0 && n_local == 1) GT(j, 4 * i + 2);
             const bool need = m_new > m_used + 8.0f;
             if (j > 0 && __any_sync(0xffffffffu, need)) {
                 const float f = need ? ptx::ex2(m_used - m_new) : 1.0f;
@@ -535,36 +570,35 @@ __global__ void __launch_bounds__(384, 1)
                 ptx::tmem_st16(tS + ch * 16, pk);
             }
             ptx::tmem_wait_st();
-            if (r == 0) GT(j, 4 * i + 3);
+            if (r == 0 && n_local == 1) GT(j, 4 * i + 3);
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar_p);
         }
 
         // ---------------------------------------------------------- epilogue
-        ptx::mbar_wait(bar_o_full, 0);
+        ptx::mbar_wait(bar_o_full0 + 8 * i, n_done & 1);
+        ++n_done;
         ptx::tc_fence_after();
+        float o[DP];
+#pragma unroll
+        for (int c = 0; c < DP / 32; ++c) ptx::tmem_ld32f(tO + c * 32, &o[c * 32]);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < DP / 32; ++c) ptx::reg_fence32(&o[c * 32]);
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(bar_o_empty0 + 8 * i);  // O_i may now be overwritten by the next item
         const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
-        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o_perm) + row_g * DP;
-#pragma unroll
-        for (int c = 0; c < DP / 32; ++c) {
-            uint32_t rr[32];
-            ptx::tmem_ld32(tO + c * 32, rr);
-            ptx::tmem_wait_ld();
-            uint32_t pk[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e)
-                pk[e] = ptx::pack_bf16x2(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
-            if (valid) {
-                uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-            }
-        }
         if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o_perm) + row_g * DP);
+#pragma unroll
+            for (int q = 0; q < DP / 8; ++q)
+                dst[q] = make_uint4(ptx::pack_bf16x2(o[8 * q] * inv_l, o[8 * q + 1] * inv_l),
+                                    ptx::pack_bf16x2(o[8 * q + 2] * inv_l, o[8 * q + 3] * inv_l),
+                                    ptx::pack_bf16x2(o[8 * q + 4] * inv_l, o[8 * q + 5] * inv_l),
+                                    ptx::pack_bf16x2(o[8 * q + 6] * inv_l, o[8 * q + 7] * inv_l));
             const float m_eff = m_used == -INFINITY ? 0.f : m_used;
             p.lse_perm[row_g] = (m_eff + __log2f(l_run)) * 0.69314718055994530942f;
         }
-        ptx::tc_fence_before();
       }
     }
 
@@ -588,7 +622,15 @@ static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CU
         configured = true;
     }
     if (n_ctas <= 0) return cudaSuccess;
-    gna_attn_sm100<DP, BV><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv);
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const long long grid = n_ctas < sms ? n_ctas : sms;  // persistent: one CTA per SM
+    gna_attn_sm100<DP, BV><<<static_cast<unsigned>(grid), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv);
     return cudaGetLastError();
 }
 

@@ -13,7 +13,8 @@ struct AttnParams {
     Geometry g;
     const int4* items;      // work list: {class, subA, subB (-1 none), kv boxes}
     long long n_items;      // items per (batch, head)
-    long long work_begin;   // global work index offset of blockIdx.x == 0
+    long long work_begin;   // global work range [work_begin, work_end) processed by the launch
+    long long work_end;
     void* o_perm;           // bf16 permuted O  [BH][C][nbox][box_vol][Dp]
     float* lse_perm;        // fp32 permuted LSE [BH][C][nbox][box_vol]
     float scale_log2;       // softmax scale * log2(e)

@@ -116,7 +116,8 @@ def make_args(batch, heads, head_dim, spatial, window, stride=None, dilation=Non
     return a
 
 
-def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags):
+def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,
+                 workspace=None):
     import torch
 
     for name, t in (("q", q), ("k", k), ("v", v), ("out", out)):
@@ -132,14 +133,19 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
     spatial = list(q.shape[1:-2])
     if stream is None:
         stream = torch.cuda.current_stream(q.device).cuda_stream
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        if not workspace.is_cuda or not workspace.is_contiguous():
+            raise GnaError("workspace must be a contiguous CUDA tensor")
+        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
     return make_args(batch, heads, head_dim, spatial, window, stride, dilation, causal, scale,
                      q=q.data_ptr(), k=k.data_ptr(), v=v.data_ptr(), out=out.data_ptr(),
                      lse=(lse.data_ptr() if lse is not None else None), stream=stream, box=box,
-                     work_range=work_range, flags=flags)
+                     work_range=work_range, flags=flags, workspace=ws_ptr, workspace_bytes=ws_bytes)
 
 
 def forward(q, k, v, window, stride=None, dilation=None, causal=None, scale=None, out=None, lse=None,
-            box=None, work_range=None, stream=None, return_lse=True, flags=0):
+            box=None, work_range=None, stream=None, return_lse=True, flags=0, workspace=None):
     """GNA forward on CUDA bf16 tensors [B, *spatial, H, D] (heads-last).
 
     Returns (out, lse) -- lse fp32 [B, *spatial, H] (natural log)."""
@@ -149,31 +155,36 @@ def forward(q, k, v, window, stride=None, dilation=None, causal=None, scale=None
         out = torch.empty_like(q)
     if lse is None and return_lse:
         lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
-    a = _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags)
+    a = _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,
+                     workspace)
     with torch.cuda.device(q.device):
         _check(load().gna_forward_ex(ctypes.byref(a)))
     return out, lse
 
 
-def _stage(fn_name, q, k, v, out, lse, window, stride, dilation, causal, scale, box, stream, flags):
+def _stage(fn_name, q, k, v, out, lse, window, stride, dilation, causal, scale, box, stream, flags,
+           workspace=None, work_range=None):
     import torch
 
-    a = _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, None, stream, flags)
+    a = _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,
+                     workspace)
     with torch.cuda.device(q.device):
         _check(getattr(load(), fn_name)(ctypes.byref(a)))
 
 
-def permute(q, k, v, out, window, stride=None, dilation=None, causal=None, box=None, stream=None):
-    _stage("gna_permute", q, k, v, out, None, window, stride, dilation, causal, None, box, stream, 0)
+def permute(q, k, v, out, window, stride=None, dilation=None, causal=None, box=None, stream=None, workspace=None):
+    _stage("gna_permute", q, k, v, out, None, window, stride, dilation, causal, None, box, stream, 0, workspace)
 
 
 def attention_permuted(q, k, v, out, window, stride=None, dilation=None, causal=None, scale=None, box=None,
-                       stream=None):
-    _stage("gna_attention_permuted", q, k, v, out, None, window, stride, dilation, causal, scale, box, stream, 0)
+                       stream=None, workspace=None, work_range=None):
+    _stage("gna_attention_permuted", q, k, v, out, None, window, stride, dilation, causal, scale, box, stream, 0,
+           workspace, work_range)
 
 
-def unpermute(q, k, v, out, lse, window, stride=None, dilation=None, causal=None, box=None, stream=None):
-    _stage("gna_unpermute", q, k, v, out, lse, window, stride, dilation, causal, None, box, stream, 0)
+def unpermute(q, k, v, out, lse, window, stride=None, dilation=None, causal=None, box=None, stream=None,
+              workspace=None):
+    _stage("gna_unpermute", q, k, v, out, lse, window, stride, dilation, causal, None, box, stream, 0, workspace)
 
 
 def plan_info(batch, heads, head_dim, spatial, window, stride=None, dilation=None, causal=None, box=None) -> dict:
