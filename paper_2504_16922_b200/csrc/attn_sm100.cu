@@ -5,12 +5,13 @@
 // the sub-tiles' analytic ranges (geom.cuh; §3.3): no mask tensor
 // ever exists in HBM, and boxes outside the range are never loaded.
 //
-// Warp roles (384 threads, registers re-balanced with setmaxnreg):
-//   warps 0-3  softmax WG0 : rows of sub-tile A, TMEM lanes 0-127, S0/P0, O0 (224 regs)
-//   warps 4-7  softmax WG1 : rows of sub-tile B, S1/P1, O1                   (224 regs)
-//   warp  8    TMA producer: Q sub-tiles once, then K_j, V_j into a smem ring (56 regs)
-//   warp  9    MMA issuer  : tcgen05.mma, one elected lane
-//   warps 10-11 idle (complete the control warpgroup for setmaxnreg)
+// Warp roles (640 threads, registers re-balanced with setmaxnreg):
+//   warps 0-7   softmax of sub-tile A: TMEM lanes 0-127, S0/P0, O0; each row is
+//               split between two threads (64 keys each)             (112 regs)
+//   warps 8-15  softmax of sub-tile B: S1/P1, O1                       (112 regs)
+//   warp  16    TMA producer: Q sub-tiles, then K_j, V_j into a smem ring (32 regs)
+//   warp  17    MMA issuer  : tcgen05.mma, one elected lane
+//   warps 18-19 idle (complete the control warpgroup for setmaxnreg)
 // TMEM (512 columns x 128 lanes, fp32):  S0 [0,128)  S1 [128,256)
 //   O0 [256, 256+Dp)  O1 [384, 384+Dp); P_i (bf16x2) aliases S_i's first 64.
 //
@@ -61,13 +62,17 @@ struct Cfg {
     static constexpr int NH = DP / 64;               // 128-byte column chunks ("halves")
     static constexpr int CHUNK_BYTES = 128 * 128;    // 128 rows x 128 B, one SW128 chunk
     static constexpr int TILE_BYTES = NH * CHUNK_BYTES;  // 128 rows x DP bf16
-    static constexpr int NS = DP == 128 ? 5 : 12;    // KV ring slots (K and V share it)
+    static constexpr int NS = DP == 128 ? 4 : 10;    // KV ring slots (K and V share it)
     static constexpr int KPB = 128 / BV;             // boxes per 128-row tile
     static constexpr int Q_OFF = 0;
     static constexpr int KV_OFF = 2 * TILE_BYTES;
     static constexpr int BAR_OFF = KV_OFF + NS * TILE_BYTES;
-    static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
-    static constexpr int THREADS = 384;
+    static constexpr int RED_OFF = BAR_OFF + 512;      // row max / row sum exchange between column halves
+    static constexpr int FULL_OFF = RED_OFF + 4096;   // per sub-tile bitmap: box of the union needs no mask
+    static constexpr int FULL_BITS = 8192;
+    static constexpr int ROW_OFF = FULL_OFF + 2 * FULL_BITS / 8;  // per-row windows / output row, per item
+    static constexpr int SMEM_BYTES = ROW_OFF + 2 * 8 * 128 * 4 + 64 + 1024;  // + item range + alignment slack
+    static constexpr int THREADS = 640;
 };
 
 // Odometer over the KV boxes of the union range [lo, hi) (row-major, last axis
@@ -101,22 +106,14 @@ __device__ __forceinline__ u128 bits_below(int n) {  // n in [0, 128]
 }
 __device__ __forceinline__ u128 bit_range(int a, int b) { return bits_below(b) & ~bits_below(a); }
 
-struct BoxMaskConsts {
-    u128 comb1;  // bit i1*B2 for i1 < B1
-    u128 comb0;  // bit i0*B1*B2 for i0 < B0
-};
-
-__device__ __forceinline__ BoxMaskConsts box_mask_consts(const Geometry& g) {
-    BoxMaskConsts c;
-    c.comb1 = 0;
-    c.comb0 = 0;
-    for (int i = 0; i < g.B[1]; ++i) c.comb1 |= static_cast<u128>(1) << (i * g.B[2]);
-    for (int i = 0; i < g.B[0]; ++i) c.comb0 |= static_cast<u128>(1) << (i * g.B[1] * g.B[2]);
+// sum_{i < n} 2^(i*step) for a power-of-two n, by doubling (<= 7 steps)
+__device__ __forceinline__ u128 comb(int n, int step) {
+    u128 c = 1;
+    for (int len = 1; len < n; len *= 2) c |= c << (len * step);
     return c;
 }
 
-__device__ __forceinline__ u128 box_row_mask(const Geometry& g, const BoxMaskConsts& mc, const int lo[3],
-                                             const int hi[3]) {
+__device__ __forceinline__ u128 box_row_mask(const Geometry& g, const int lo[3], const int hi[3]) {
     int a[3], b[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -125,9 +122,9 @@ __device__ __forceinline__ u128 box_row_mask(const Geometry& g, const BoxMaskCon
         if (a[k] >= b[k]) return 0;
     }
     const u128 m2 = bit_range(a[2], b[2]);
-    const u128 m12 = (m2 * mc.comb1) & bit_range(a[1] * g.B[2], b[1] * g.B[2]);
+    const u128 m12 = (m2 * comb(g.B[1], g.B[2])) & bit_range(a[1] * g.B[2], b[1] * g.B[2]);
     const int s01 = g.B[1] * g.B[2];
-    return (m12 * mc.comb0) & bit_range(a[0] * s01, b[0] * s01);
+    return (m12 * comb(g.B[0], s01)) & bit_range(a[0] * s01, b[0] * s01);
 }
 
 }  // namespace
@@ -169,7 +166,7 @@ __device__ __forceinline__ void load_item(const AttnParams& p, long long w, Work
 // warp starts the next item's QK^T while the softmax warps run the epilogue, and
 // the first PV of the next item waits only for the epilogue's TMEM read (o_empty).
 template <int DP, int BV>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(640, 1)
     gna_attn_sm100(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v) {
     using C = Cfg<DP, BV>;
@@ -206,13 +203,13 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(bar_s_full0 + 8 * i, 1);
-            ptx::mbar_init(bar_p_full0 + 8 * i, 128);
+            ptx::mbar_init(bar_p_full0 + 8 * i, 256);
             ptx::mbar_init(bar_o_full0 + 8 * i, 1);
-            ptx::mbar_init(bar_o_empty0 + 8 * i, 128);
+            ptx::mbar_init(bar_o_empty0 + 8 * i, 256);
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 8) {
+    if (warp == 16) {
         ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
         ptx::tmem_relinquish();
     }
@@ -221,9 +218,9 @@ __global__ void __launch_bounds__(384, 1)
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
 
-    if (warp >= 8) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
-      if (warp == 8) {
+    if (warp >= 16) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n" ::: "memory");
+      if (warp == 16) {
         // ===================================================== TMA producer
         if (lane == 0) {
             ptx::tma_prefetch_desc(&tmap_q);
@@ -285,7 +282,7 @@ __global__ void __launch_bounds__(384, 1)
                 ++n_local;
             }
         }
-      } else if (warp == 9) {
+      } else if (warp == 17) {
         // ======================================================= MMA issuer
         if (lane == 0) {
             constexpr uint32_t IDESC_QK = ptx::idesc_bf16(128, 128, 0, 0);
@@ -381,17 +378,24 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     } else {
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
-      // ==================================================== softmax WG i
-      const int i = warp >> 2;
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n" ::: "memory");
+      // ==================================================== softmax
+      // 16 warps: sub-tile i = warp / 8; within a sub-tile, warp & 3 selects the TMEM
+      // lane quarter (rows) and (warp / 4) & 1 the column half: every row is shared by
+      // two threads (64 keys each), halving the softmax latency that sits on the
+      // S -> P -> PV -> S critical path.  Row max and row sum are exchanged in smem.
+      const int i = warp >> 3;
+      const int hh = (warp >> 2) & 1;
       const int wl = warp & 3;
-      const int r = threadIdx.x & 127;  // row of the sub-tile == TMEM lane
+      const int r = wl * 32 + lane;  // row of the sub-tile == TMEM lane
       const uint32_t lane_off = static_cast<uint32_t>(wl * 32) << 16;
-      const uint32_t tS = tmem + i * 128 + lane_off;
-      const uint32_t tO = tmem + 256 + i * 128 + lane_off;
+      const uint32_t tS = tmem + i * 128 + lane_off + hh * 64;           // my 64 S columns
+      const uint32_t tP = tmem + i * 128 + lane_off + hh * 32;           // my 32 bf16x2 P columns
+      const uint32_t tO = tmem + 256 + i * 128 + lane_off + hh * (DP / 2);  // my DP/2 O columns
       const uint32_t bar_s = bar_s_full0 + 8 * i;
       const uint32_t bar_p = bar_p_full0 + 8 * i;
-      const BoxMaskConsts mconst = box_mask_consts(g);
+      float* red_m = reinterpret_cast<float*>(sgen + C::RED_OFF) + i * 256;  // [half][row]
+      float* red_l = red_m + 512;
       const float sl2 = p.scale_log2;
       int cnt_s = 0, n_done = 0, n_local = 0;
       WorkItem wi;
@@ -425,95 +429,124 @@ __global__ void __launch_bounds__(384, 1)
             }
             window(g.ax[a], Lc, x, &wst[a], &wen[a]);
         }
-        const long long row_g =
-            wi.cls_row0 + static_cast<long long>((bx[0] * g.nb[1] + bx[1]) * g.nb[2] + bx[2]) * BV + inner;
-
-        // Uniform (per sub-tile) coverage bits per axis over the union range: bit
-        // (k - lo[a]) set iff every in-bounds query of the sub-tile attends every key
-        // of box k on axis a (and the box is inside the class extent).  A stage needs
-        // no mask iff all its boxes are covered on all three axes.
-        uint64_t fullbits[3];
-        {
-            const bool fits = hi[0] - lo[0] <= 64 && hi[1] - lo[1] <= 64 && hi[2] - lo[2] <= 64;
+        // Per-row data needed only off the hot path (mask construction, epilogue) lives
+        // in shared memory, keeping the stage loop inside the 112-register budget.
+        int* rowinfo = reinterpret_cast<int*>(sgen + C::ROW_OFF) + i * 8 * 128;  // [field][row]
+        int* itemrng = reinterpret_cast<int*>(sgen + C::ROW_OFF + 2 * 8 * 128 * 4) + i * 8;
+        if (hh == 0) {
+            const long long row_g =
+                valid ? wi.cls_row0 + static_cast<long long>((bx[0] * g.nb[1] + bx[1]) * g.nb[2] + bx[2]) * BV + inner
+                      : -1;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const int Lc = class_extent(g.ax[a], cc[a]);
-                const int x0 = sc[a] * g.QB[a] * g.B[a], x1 = x0 + g.QB[a] * g.B[a];
-                uint64_t bits = 0;
-                if (fits)
-                    for (int k = lo[a]; k < hi[a]; ++k)
-                        if (box_full(g.ax[a], Lc, x0, x1, k, g.B[a])) bits |= 1ull << (k - lo[a]);
-                fullbits[a] = bits;
+                rowinfo[a * 128 + r] = wst[a];
+                rowinfo[(3 + a) * 128 + r] = wen[a];
             }
+            rowinfo[6 * 128 + r] = static_cast<int>(row_g & 0xffffffffll);
+            rowinfo[7 * 128 + r] = static_cast<int>(row_g >> 32);
+            if (r == 0)
+                for (int a = 0; a < 3; ++a) {
+                    itemrng[a] = lo[a];
+                    itemrng[3 + a] = hi[a];
+                }
+        }
+
+        // Per sub-tile bitmap over the union's boxes (row-major box index b): bit b set
+        // iff every in-bounds query of the sub-tile attends every key of box b and the
+        // box lies inside the class extent -- the uniform "full tile" predicate
+        // (P:628-630), computed once per item by the sub-tile's 256 threads (one 32-box
+        // word each).  Unions larger than FULL_BITS boxes are always masked.
+        uint32_t* fullmap = reinterpret_cast<uint32_t*>(sgen + C::FULL_OFF) + i * (C::FULL_BITS / 32);
+        {
+            const int t = (warp & 7) * 32 + lane;
+            const int ext1 = hi[1] - lo[1], ext2 = hi[2] - lo[2];
+            int Lc[3], x0[3], x1[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                Lc[a] = class_extent(g.ax[a], cc[a]);
+                x0[a] = sc[a] * g.QB[a] * g.B[a];
+                x1[a] = x0[a] + g.QB[a] * g.B[a];
+            }
+            for (int wd = t; wd < C::FULL_BITS / 32; wd += 256) {
+                uint32_t word = 0;
+                if (nkv <= C::FULL_BITS)
+                    for (int e = 0; e < 32; ++e) {
+                        const int b = wd * 32 + e;
+                        if (b >= nkv) break;
+                        const int k2 = lo[2] + b % ext2, k1 = lo[1] + (b / ext2) % ext1, k0 = lo[0] + b / (ext2 * ext1);
+                        if (box_full(g.ax[0], Lc[0], x0[0], x1[0], k0, g.B[0]) &&
+                            box_full(g.ax[1], Lc[1], x0[1], x1[1], k1, g.B[1]) &&
+                            box_full(g.ax[2], Lc[2], x0[2], x1[2], k2, g.B[2]))
+                            word |= 1u << e;
+                    }
+                fullmap[wd] = word;
+            }
+            asm volatile("bar.sync %0, 256;" ::"r"(1 + i) : "memory");
         }
         float m_used = -INFINITY;
         float l_run = 0.f;
-        BoxIter bi;
-        bi.init(lo);
         for (int j = 0; j < nst; ++j) {
-            int kb[KPB][3];
-            bool stage_full = true;
+            // the box holding my 64 keys: box hh of the stage (box_vol 64) or the single box
+            const int my_box = j * KPB + (KPB == 2 ? hh : 0);
+            const bool live = my_box < nkv;
+            const bool my_full = live && ((fullmap[my_box >> 5] >> (my_box & 31)) & 1u);
+            // row mask over my 64 keys (built before S is loaded, to keep it off the
+            // register peak); filler boxes mask everything
+            uint64_t msk = 0;
+            if (!my_full && live) {
+                const volatile int* ir = itemrng;
+                const int l0 = ir[0], l1 = ir[1], l2 = ir[2];
+                const int ext1 = ir[4] - l1, ext2 = ir[5] - l2;
+                const int kb[3] = {l0 + my_box / (ext2 * ext1), l1 + (my_box / ext2) % ext1, l2 + my_box % ext2};
+                int rlo[3], rhi[3];
 #pragma unroll
-            for (int u = 0; u < KPB; ++u) {
-                const bool live = j * KPB + u < nkv;
-#pragma unroll
-                for (int a = 0; a < 3; ++a) kb[u][a] = bi.k[a];
-                stage_full = stage_full && live && ((fullbits[0] >> (bi.k[0] - lo[0])) & (fullbits[1] >> (bi.k[1] - lo[1])) &
-                                                    (fullbits[2] >> (bi.k[2] - lo[2])) & 1ull);
-                if (live) bi.next(lo, hi);
-                else kb[u][0] = -(1 << 20);  // filler: no key of it is ever inside a window
+                for (int a = 0; a < 3; ++a) {
+                    rlo[a] = rowinfo[a * 128 + r] - kb[a] * g.B[a];
+                    rhi[a] = rowinfo[(3 + a) * 128 + r] - kb[a] * g.B[a];
+                }
+                const u128 bm = box_row_mask(g, rlo, rhi);
+                msk = static_cast<uint64_t>(KPB == 1 ? (bm >> (64 * hh)) : bm);
             }
 
             ptx::mbar_wait(bar_s, cnt_s & 1);
             ++cnt_s;
-            if (r == 0 && n_local == 1) GT(j, 4 * i + 0);
+            if (r == 0 && hh == 0 && n_local == 1) GT(j, 4 * i + 0);
             ptx::tc_fence_after();
-            float s[128];
+            // pass 1: row max over my 64 keys (two 32-column TMEM loads, masked)
+            float m_half;
+            {
+                float s[64];
+                ptx::tmem_ld32f(tS, &s[0]);
+                ptx::tmem_ld32f(tS + 32, &s[32]);
+                ptx::tmem_wait_ld();
+                ptx::reg_fence32(&s[0]);
+                ptx::reg_fence32(&s[32]);
+                if (r == 0 && hh == 0 && n_local == 1) GT(j, 4 * i + 1);
+                if (!my_full) {
+                    const uint32_t mw[2] = {static_cast<uint32_t>(msk), static_cast<uint32_t>(msk >> 32)};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) ptx::tmem_ld32f(tS + c * 32, &s[c * 32]);
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 4; ++c) ptx::reg_fence32(&s[c * 32]);
-            if (r == 0 && n_local == 1) GT(j, 4 * i + 1);
-            if (!stage_full) {
-                // 128-bit row mask of the stage (1 or 2 boxes), then one select per element
-                int rlo[3], rhi[3];
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    rlo[a] = wst[a] - kb[0][a] * g.B[a];
-                    rhi[a] = wen[a] - kb[0][a] * g.B[a];
+                    for (int c = 0; c < 64; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
                 }
-                u128 m = box_row_mask(g, mconst, rlo, rhi);
-                if (KPB == 2) {
+                float mx[8];
 #pragma unroll
-                    for (int a = 0; a < 3; ++a) {
-                        rlo[a] = wst[a] - kb[KPB - 1][a] * g.B[a];
-                        rhi[a] = wen[a] - kb[KPB - 1][a] * g.B[a];
-                    }
-                    m |= box_row_mask(g, mconst, rlo, rhi) << 64;
+                for (int e = 0; e < 8; ++e) mx[e] = s[e];
+#pragma unroll
+                for (int c = 8; c < 64; c += 16) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) mx[e] = ptx::max3(mx[e], s[c + 2 * e], s[c + 2 * e + 1]);
                 }
-                const uint32_t mw[4] = {static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32),
-                                        static_cast<uint32_t>(m >> 64), static_cast<uint32_t>(m >> 96)};
-#pragma unroll
-                for (int c = 0; c < 128; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
+                m_half = ptx::max3(ptx::max3(mx[0], mx[1], mx[2]), ptx::max3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
             }
-            float mx[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) mx[e] = s[e];
-#pragma unroll
-            for (int c = 8; c < 128; c += 16) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) mx[e] = ptx::max3(mx[e], s[c + 2 * e], s[c + 2 * e + 1]);
-            }
-            const float m_tile =
-                ptx::max3(ptx::max3(mx[0], mx[1], mx[2]), ptx::max3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * sl2;
+            red_m[hh * 128 + r] = m_half;
+            asm volatile("bar.sync %0, 256;" ::"r"(1 + i) : "memory");
+            const float m_tile = fmaxf(m_half, red_m[(hh ^ 1) * 128 + r]) * sl2;
             const float m_new = fmaxf(m_used, m_tile);
-            if (r == 0 && n_local == 1) GT(j, 4 * i + 2);
+            if (r == 0 && hh == 0 && n_local == 1) GT(j, 4 * i + 2);
             const bool need = m_new > m_used + 8.0f;
             if (j > 0 && __any_sync(0xffffffffu, need)) {
                 const float f = need ? ptx::ex2(m_used - m_new) : 1.0f;
 #pragma unroll
-                for (int c = 0; c < DP / 32; ++c) {
+                for (int c = 0; c < DP / 64; ++c) {
                     uint32_t rr[32];
                     ptx::tmem_ld32(tO + c * 32, rr);
                     ptx::tmem_wait_ld();
@@ -527,50 +560,47 @@ __global__ void __launch_bounds__(384, 1)
                 m_used = m_new;
             }
             const float neg = m_used == -INFINITY ? 0.f : -m_used;
-            // In separate, fully unrolled phases so the MUFU stream is back to back:
-            // x = s * scale*log2(e) - m (FFMA2); 2^x on MUFU for 3 pairs in 4 and on
-            // the FMA pipe (polynomial) for the 4th; row sum with 8 FADD2 chains; bf16x2
-            // pack and TMEM store in four 16-column chunks.
+            // pass 2, per 32 keys: reload S from TMEM (keeps the live set small), mask,
+            // x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU for 3 pairs in 4 and on the FMA
+            // pipe (polynomial) for the 4th (scripts/micro/exp_phase.cu), row sum (FADD2),
+            // bf16x2 pack, TMEM store of 16 P columns.
+            float la[4] = {0.f, 0.f, 0.f, 0.f}, lb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int pi = 0; pi < 64; ++pi)
-                ptx::ffma2(s[2 * pi], s[2 * pi + 1], s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
+            for (int ch = 0; ch < 2; ++ch) {
+                float s[32];
+                ptx::tmem_ld32f(tS + ch * 32, s);
+                ptx::tmem_wait_ld();
+                ptx::reg_fence32(s);
+                if (!my_full) {
+                    const uint32_t mw = static_cast<uint32_t>(msk >> (32 * ch));
 #pragma unroll
-            for (int pi = 0; pi < 64; ++pi) {
-                if ((pi & 3) == 3) {  // 1 pair in 4 on the FMA pipe (scripts/micro/exp_phase.cu: best split)
-                    ptx::ex2_poly2(s[2 * pi], s[2 * pi + 1], s[2 * pi], s[2 * pi + 1]);
-                } else {
-                    s[2 * pi] = ptx::ex2(s[2 * pi]);
-                    s[2 * pi + 1] = ptx::ex2(s[2 * pi + 1]);
-                }
-            }
-            {
-                float la[8], lb[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    la[e] = s[2 * e];
-                    lb[e] = s[2 * e + 1];
+                    for (int c = 0; c < 32; ++c) s[c] = ((mw >> c) & 1u) ? s[c] : -INFINITY;
                 }
 #pragma unroll
-                for (int pi = 8; pi < 64; pi += 8) {
+                for (int pi = 0; pi < 16; ++pi)
+                    ptx::ffma2(s[2 * pi], s[2 * pi + 1], s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        ptx::fadd2(la[e], lb[e], la[e], lb[e], s[2 * (pi + e)], s[2 * (pi + e) + 1]);
+                for (int pi = 0; pi < 16; ++pi) {
+                    if ((pi & 3) == 3) {
+                        ptx::ex2_poly2(s[2 * pi], s[2 * pi + 1], s[2 * pi], s[2 * pi + 1]);
+                    } else {
+                        s[2 * pi] = ptx::ex2(s[2 * pi]);
+                        s[2 * pi + 1] = ptx::ex2(s[2 * pi + 1]);
+                    }
                 }
 #pragma unroll
-                for (int e = 0; e < 4; ++e) ptx::fadd2(la[e], lb[e], la[e], lb[e], la[e + 4], lb[e + 4]);
-                ptx::fadd2(la[0], lb[0], la[0], lb[0], la[2], lb[2]);
-                ptx::fadd2(la[1], lb[1], la[1], lb[1], la[3], lb[3]);
-                l_run += (la[0] + lb[0]) + (la[1] + lb[1]);
-            }
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {  // 32 columns -> 16 packed bf16x2 TMEM columns per chunk
+                for (int pi = 0; pi < 16; ++pi)
+                    ptx::fadd2(la[pi & 3], lb[pi & 3], la[pi & 3], lb[pi & 3], s[2 * pi], s[2 * pi + 1]);
                 uint32_t pk[16];
 #pragma unroll
-                for (int q = 0; q < 16; ++q) pk[q] = ptx::pack_bf16x2(s[ch * 32 + 2 * q], s[ch * 32 + 2 * q + 1]);
-                ptx::tmem_st16(tS + ch * 16, pk);
+                for (int q = 0; q < 16; ++q) pk[q] = ptx::pack_bf16x2(s[2 * q], s[2 * q + 1]);
+                ptx::tmem_st16(tP + ch * 16, pk);
             }
+            ptx::fadd2(la[0], lb[0], la[0], lb[0], la[2], lb[2]);
+            ptx::fadd2(la[1], lb[1], la[1], lb[1], la[3], lb[3]);
+            l_run += (la[0] + lb[0]) + (la[1] + lb[1]);
             ptx::tmem_wait_st();
-            if (r == 0 && n_local == 1) GT(j, 4 * i + 3);
+            if (r == 0 && hh == 0 && n_local == 1) GT(j, 4 * i + 3);
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar_p);
         }
@@ -579,31 +609,38 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_wait(bar_o_full0 + 8 * i, n_done & 1);
         ++n_done;
         ptx::tc_fence_after();
-        float o[DP];
+        float o[DP / 2];
 #pragma unroll
-        for (int c = 0; c < DP / 32; ++c) ptx::tmem_ld32f(tO + c * 32, &o[c * 32]);
+        for (int c = 0; c < DP / 64; ++c) ptx::tmem_ld32f(tO + c * 32, &o[c * 32]);
         ptx::tmem_wait_ld();
 #pragma unroll
-        for (int c = 0; c < DP / 32; ++c) ptx::reg_fence32(&o[c * 32]);
+        for (int c = 0; c < DP / 64; ++c) ptx::reg_fence32(&o[c * 32]);
         ptx::tc_fence_before();
         ptx::mbar_arrive(bar_o_empty0 + 8 * i);  // O_i may now be overwritten by the next item
-        const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
-        if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o_perm) + row_g * DP);
+        red_l[hh * 128 + r] = l_run;
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + i) : "memory");
+        const float l_tot = l_run + red_l[(hh ^ 1) * 128 + r];
+        const float inv_l = l_tot > 0.f ? 1.0f / l_tot : 0.f;
+        const long long row_g = static_cast<long long>(static_cast<unsigned>(rowinfo[6 * 128 + r])) |
+                                (static_cast<long long>(rowinfo[7 * 128 + r]) << 32);
+        if (row_g >= 0) {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p.o_perm) + row_g * DP + hh * (DP / 2));
 #pragma unroll
-            for (int q = 0; q < DP / 8; ++q)
+            for (int q = 0; q < DP / 16; ++q)
                 dst[q] = make_uint4(ptx::pack_bf16x2(o[8 * q] * inv_l, o[8 * q + 1] * inv_l),
                                     ptx::pack_bf16x2(o[8 * q + 2] * inv_l, o[8 * q + 3] * inv_l),
                                     ptx::pack_bf16x2(o[8 * q + 4] * inv_l, o[8 * q + 5] * inv_l),
                                     ptx::pack_bf16x2(o[8 * q + 6] * inv_l, o[8 * q + 7] * inv_l));
-            const float m_eff = m_used == -INFINITY ? 0.f : m_used;
-            p.lse_perm[row_g] = (m_eff + __log2f(l_run)) * 0.69314718055994530942f;
+            if (hh == 0) {
+                const float m_eff = m_used == -INFINITY ? 0.f : m_used;
+                p.lse_perm[row_g] = (m_eff + __log2f(l_tot)) * 0.69314718055994530942f;
+            }
         }
       }
     }
 
     __syncthreads();
-    if (warp == 8) {
+    if (warp == 16) {
         __syncwarp();
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, 512);
