@@ -29,8 +29,10 @@
  *      ranges, TMA + mbarrier pipeline, tcgen05 MMAs with TMEM
  *      accumulators, online softmax, fine-grained mask only on partial tiles
  *      (P:627-630); O + LSE epilogue;
- *   3. inverse permute (gna_unpermute): O, LSE back to the user layout,
- *      padding cropped.
+ *   3. inverse permute: O, LSE back to the user layout, padding cropped
+ *       -- fused into the attention epilogue by gna_forward /
+ *      gna_forward_ex (each row is scattered to its token), or run as the
+ *      separate gna_unpermute kernel after gna_attention_permuted.
  *
  * Conventions
  *   - Return codes: GNA_OK, GNA_EINVAL (argument; nothing is launched),
@@ -68,7 +70,10 @@ extern "C" {
 #define GNA_DTYPE_BF16 0
 
 /* flags */
-#define GNA_FLAG_SYNC_CHECK 1 /* synchronize + check after each launch (debug) */
+#define GNA_FLAG_SYNC_CHECK 1        /* synchronize + check after each launch (debug) */
+#define GNA_FLAG_UNFUSED_EPILOGUE 2  /* gna_forward_ex: write permuted O then run the separate
+                                        inverse-permute kernel (default: the attention epilogue
+                                        writes O and LSE straight into the user layout) */
 
 typedef struct gna_args {
     const void *q, *k, *v; /* device bf16 [B][s0][s1][s2][H][D] */

@@ -497,7 +497,7 @@ int do_permute(const gna_args* a, Ctx& c) {
     return post_launch(a, c.st, "permute_qkv");
 }
 
-int do_attention(const gna_args* a, Ctx& c) {
+int do_attention(const gna_args* a, Ctx& c, bool fused_out = false) {
     int rc;
     int4* items = nullptr;
     if ((rc = plan_device_items(*c.plan, &items))) return rc;
@@ -520,6 +520,8 @@ int do_attention(const gna_args* a, Ctx& c) {
     p.lse_perm = reinterpret_cast<float*>(c.ws + c.L.lse);
     const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));
     p.scale_log2 = scale * 1.4426950408889634f;
+    p.out_nat = fused_out ? a->out : nullptr;
+    p.lse_nat = fused_out ? a->lse : nullptr;
     GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, we - wb, c.st));
     return post_launch(a, c.st, "gna_attn_sm100");
 }
@@ -542,8 +544,11 @@ int gna_forward_ex(const gna_args* a) {
     int rc = prepare(a, true, &c);
     if (rc) return rc;
     if ((rc = do_permute(a, c))) return rc;
-    if ((rc = do_attention(a, c))) return rc;
-    return do_unpermute(a, c);
+    if (a->flags & GNA_FLAG_UNFUSED_EPILOGUE) {
+        if ((rc = do_attention(a, c))) return rc;
+        return do_unpermute(a, c);
+    }
+    return do_attention(a, c, /*fused_out=*/true);  // epilogue scatters O, LSE to the user layout
 }
 
 int gna_forward(const void* q, const void* k, const void* v, void* out, float* lse, int batch, int heads,

@@ -471,7 +471,28 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_wait(bar_o_full, 0);
         ptx::tc_fence_after();
         const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
-        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o_perm) + row_g * DP;
+        // Output row: the permuted O row (stage API), or -- fused inverse permutation
+        // -- the row of this token in the user's heads-last
+        // layout [B][s0][s1][s2][H][D], so no separate unpermute pass is needed.
+        __nv_bfloat16* orow;
+        float* lrow;
+        int ncols;
+        if (p.out_nat != nullptr) {
+            long long tok = 0;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                tok = tok * g.ax[a].L + (cc[a] + static_cast<long long>(g.ax[a].d) * (bx[a] * g.B[a] + xin[a]));
+            const long long N = static_cast<long long>(g.ax[0].L) * g.ax[1].L * g.ax[2].L;
+            const long long b = bh / g.heads, h = bh % g.heads;
+            const long long nat = (b * N + tok) * g.heads + h;
+            orow = reinterpret_cast<__nv_bfloat16*>(p.out_nat) + nat * g.D;
+            lrow = p.lse_nat != nullptr ? p.lse_nat + nat : nullptr;
+            ncols = g.D;
+        } else {
+            orow = reinterpret_cast<__nv_bfloat16*>(p.o_perm) + row_g * DP;
+            lrow = p.lse_perm + row_g;
+            ncols = DP;
+        }
 #pragma unroll
         for (int c = 0; c < DP / 32; ++c) {
             uint32_t rr[32];
@@ -481,15 +502,15 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e)
                 pk[e] = ptx::pack_bf16x2(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
-            if (valid) {
+            if (valid && c * 32 < ncols) {
                 uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
         }
-        if (valid) {
+        if (valid && lrow != nullptr) {
             const float m_eff = m_used == -INFINITY ? 0.f : m_used;
-            p.lse_perm[row_g] = (m_eff + __log2f(l_run)) * 0.69314718055994530942f;
+            *lrow = (m_eff + __log2f(l_run)) * 0.69314718055994530942f;
         }
         ptx::tc_fence_before();
       }

@@ -18,6 +18,8 @@ struct AttnParams {
     void* o_perm;           // bf16 permuted O  [BH][C][nbox][box_vol][Dp]
     float* lse_perm;        // fp32 permuted LSE [BH][C][nbox][box_vol]
     float scale_log2;       // softmax scale * log2(e)
+    void* out_nat;          // if non-null: fused inverse permutation, O written to the user layout
+    float* lse_nat;         //   and LSE likewise (may be null)
 };
 
 // Permuted layout sizes (rows of Dp elements)

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("GNA_LIB_PATH") or os.path.join(_HERE, "libgna_b200.so
 GNA_OK, GNA_EINVAL, GNA_EUNSUPPORTED, GNA_ECUDA, GNA_ENOMEM = range(5)
 GNA_DTYPE_BF16 = 0
 GNA_FLAG_SYNC_CHECK = 1
+GNA_FLAG_UNFUSED_EPILOGUE = 2
 
 _I3 = ctypes.c_int * 3
 

@@ -179,6 +179,21 @@ def test_stages_equal_forward(gna):
     assert torch.equal(out, o2) and torch.equal(lse, l2)
 
 
+def test_fused_epilogue_equals_unfused_path(gna):
+    """The default forward scatters O/LSE from the attention epilogue (fused inverse
+    permutation); GNA_FLAG_UNFUSED_EPILOGUE runs the separate unpermute kernel.
+    Both must agree bit for bit, for every head_dim (D=32 is padded to 64)."""
+    from paper_2504_16922_b200.gna import GNA_FLAG_UNFUSED_EPILOGUE
+
+    for cfg, D in ((SMALL[3], 128), (SMALL[4], 64), (SMALL[1], 32)):
+        q, k, v = (t.cuda() for t in make_qkv(2, cfg["spatial"], 3, D))
+        o1, l1 = gna.forward(q, k, v, cfg["window"], cfg["stride"], cfg["dilation"], cfg["causal"])
+        o2, l2 = gna.forward(q, k, v, cfg["window"], cfg["stride"], cfg["dilation"], cfg["causal"],
+                             flags=GNA_FLAG_UNFUSED_EPILOGUE)
+        torch.cuda.synchronize()
+        assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
 def test_work_range_split_is_bitwise(gna):
     """Q-tile splitting (multi-GPU sharding) over [begin, end) ranges of the work
     list reproduces the single launch bit for bit."""
