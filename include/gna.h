@@ -22,7 +22,15 @@
  *   1-D problems pass spatial = {L, 1, 1}; unused axes must be exactly
  *   window = stride = dilation = 1, causal = 0.
  *
- * Pipeline behind gna_forward (§3.3, re-designed for sm_100a):
+ * Default path of gna_forward / gna_forward_ex (permute-free):
+ * ONE kernel -- the attention kernel gathers each multi-dimensional Q/KV box
+ * (one dilation class, one head) straight from the user tensors with 5-D TMA
+ * loads (element stride = dilation, hardware zero fill past the edges) and
+ * scatters O / LSE rows back from its epilogue.  Used when head_dim >= 64 and
+ * box*dilation <= 256 per axis; otherwise, or with GNA_FLAG_PERMUTED, the
+ * three-step pipeline below runs.
+ *
+ * Permuted pipeline (§3.3, re-designed for sm_100a):
  *   1. token permute (gna_permute): Q, K, V -> tile-contiguous boxes, per
  *      dilation class, zero-padded;
  *   2. fused attention (gna_attention_permuted): analytic per-Q-tile KV box
@@ -74,6 +82,8 @@ extern "C" {
 #define GNA_FLAG_UNFUSED_EPILOGUE 2  /* gna_forward_ex: write permuted O then run the separate
                                         inverse-permute kernel (default: the attention epilogue
                                         writes O and LSE straight into the user layout) */
+#define GNA_FLAG_PERMUTED 4          /* gna_forward_ex: use the permute -> attention path even when
+                                        the permute-free (direct 5-D TMA) path is available */
 
 typedef struct gna_args {
     const void *q, *k, *v; /* device bf16 [B][s0][s1][s2][H][D] */

@@ -450,6 +450,33 @@ int make_tmap(CUtensorMap* m, const void* base, const Geometry& g) {
     return GNA_OK;
 }
 
+// 5-D map over a user tensor [B][s0][s1][s2][H][D] (direct, permute-free mode):
+// dims (D, H, s2, s1, B*s0), box {64, 1, B2*d2, B1*d1, B0*d0}, element strides
+// (1, 1, d2, d1, d0): one box load gathers the box of one dilation class of one head.
+int make_tmap_direct(CUtensorMap* m, const void* base, const Geometry& g, bool* ok) {
+    *ok = false;
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    if (g.D < 64) return GNA_OK;
+    for (int a = 0; a < 3; ++a)
+        if (g.B[a] * g.ax[a].d > 256 || g.ax[a].d > 8) return GNA_OK;
+    const cuuint64_t D = g.D, H = g.heads;
+    cuuint64_t dims[5] = {D, H, static_cast<cuuint64_t>(g.ax[2].L), static_cast<cuuint64_t>(g.ax[1].L),
+                          static_cast<cuuint64_t>(g.batch) * g.ax[0].L};
+    cuuint64_t strides[4] = {D * 2, H * D * 2, g.ax[2].L * H * D * 2,
+                             static_cast<cuuint64_t>(g.ax[1].L) * g.ax[2].L * H * D * 2};
+    cuuint32_t box[5] = {64, 1, static_cast<cuuint32_t>(g.B[2] * g.ax[2].d), static_cast<cuuint32_t>(g.B[1] * g.ax[1].d),
+                         static_cast<cuuint32_t>(g.B[0] * g.ax[0].d)};
+    cuuint32_t estr[5] = {1, 1, static_cast<cuuint32_t>(g.ax[2].d), static_cast<cuuint32_t>(g.ax[1].d),
+                          static_cast<cuuint32_t>(g.ax[0].d)};
+    if (dims[4] >= (1ull << 31)) return GNA_OK;
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    *ok = r == CUDA_SUCCESS;
+    return GNA_OK;
+}
+
 int check_device() {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -479,7 +506,7 @@ struct Ctx {
     cudaStream_t st = nullptr;
 };
 
-int prepare(const gna_args* a, bool need_ptrs, Ctx* c) {
+int prepare(const gna_args* a, bool need_ptrs, Ctx* c, bool need_ws = true) {
     int rc = validate(a, need_ptrs);
     if (rc) return rc;
     if ((rc = check_device())) return rc;
@@ -489,6 +516,7 @@ int prepare(const gna_args* a, bool need_ptrs, Ctx* c) {
     c->g.heads = a->heads;
     c->L = ws_layout(c->g);
     c->st = static_cast<cudaStream_t>(a->stream);
+    if (!need_ws) return GNA_OK;
     return get_workspace(a, c->L.total, &c->ws);
 }
 
@@ -497,15 +525,23 @@ int do_permute(const gna_args* a, Ctx& c) {
     return post_launch(a, c.st, "permute_qkv");
 }
 
-int do_attention(const gna_args* a, Ctx& c, bool fused_out = false) {
+int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct = false,
+                 const CUtensorMap* direct_maps = nullptr) {
     int rc;
     int4* items = nullptr;
     if ((rc = plan_device_items(*c.plan, &items))) return rc;
     CUtensorMap tq, tk, tv;
-    if ((rc = make_tmap(&tq, c.ws + c.L.q, c.g))) return rc;
-    if ((rc = make_tmap(&tk, c.ws + c.L.k, c.g))) return rc;
-    if ((rc = make_tmap(&tv, c.ws + c.L.v, c.g))) return rc;
+    if (direct) {
+        tq = direct_maps[0];
+        tk = direct_maps[1];
+        tv = direct_maps[2];
+    } else {
+        if ((rc = make_tmap(&tq, c.ws + c.L.q, c.g))) return rc;
+        if ((rc = make_tmap(&tk, c.ws + c.L.k, c.g))) return rc;
+        if ((rc = make_tmap(&tv, c.ws + c.L.v, c.g))) return rc;
+    }
     AttnParams p{};
+    p.direct = direct ? 1 : 0;
     p.g = c.g;
     p.items = items;
     p.n_items = static_cast<long long>(c.plan->items.size());
@@ -516,8 +552,8 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false) {
     if (wb > we) return fail(GNA_EINVAL, "work_begin > work_end");
     p.work_begin = wb;
     p.work_end = we;
-    p.o_perm = c.ws + c.L.o;
-    p.lse_perm = reinterpret_cast<float*>(c.ws + c.L.lse);
+    p.o_perm = c.ws ? c.ws + c.L.o : nullptr;
+    p.lse_perm = c.ws ? reinterpret_cast<float*>(c.ws + c.L.lse) : nullptr;
     const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out_nat = fused_out ? a->out : nullptr;
@@ -541,8 +577,19 @@ extern "C" {
 
 int gna_forward_ex(const gna_args* a) {
     Ctx c;
-    int rc = prepare(a, true, &c);
+    int rc = prepare(a, true, &c, /*need_ws=*/false);
     if (rc) return rc;
+    if (!(a->flags & (GNA_FLAG_PERMUTED | GNA_FLAG_UNFUSED_EPILOGUE))) {
+        // permute-free path: one kernel, 5-D TMA boxes straight from the user tensors,
+        // O and LSE scattered by the epilogue
+        CUtensorMap maps[3];
+        bool ok[3];
+        if ((rc = make_tmap_direct(&maps[0], a->q, c.g, &ok[0]))) return rc;
+        if ((rc = make_tmap_direct(&maps[1], a->k, c.g, &ok[1]))) return rc;
+        if ((rc = make_tmap_direct(&maps[2], a->v, c.g, &ok[2]))) return rc;
+        if (ok[0] && ok[1] && ok[2]) return do_attention(a, c, /*fused_out=*/true, /*direct=*/true, maps);
+    }
+    if ((rc = get_workspace(a, c.L.total, &c.ws))) return rc;
     if ((rc = do_permute(a, c))) return rc;
     if (a->flags & GNA_FLAG_UNFUSED_EPILOGUE) {
         if ((rc = do_attention(a, c))) return rc;

@@ -217,6 +217,29 @@ __global__ void __launch_bounds__(384, 1)
             ptx::tma_prefetch_desc(&tmap_q);
             ptx::tma_prefetch_desc(&tmap_k);
             ptx::tma_prefetch_desc(&tmap_v);
+            // One box of 64/128 token rows, both D halves.  Permuted mode: a contiguous row
+            // range of the permuted tensor (2-D map).  Direct mode (permute-free, SURVEY
+            // NEXT-2): a 5-D box {64 cols, 1 head, B2, B1, B0 tokens} of the user's
+            // heads-last tensor with element strides = dilation, so the TMA gathers the
+            // class sub-grid itself and zero-fills past the tensor edges.
+            const long long b_idx = bh / g.heads;
+            const int h_idx = static_cast<int>(bh % g.heads);
+            int ccls[3];
+            class_coords(g, cls, ccls);
+            auto load_box = [&](const CUtensorMap* tm, uint32_t dst, uint32_t bar, int k0, int k1, int k2) {
+                if (p.direct) {
+                    const int c2 = ccls[2] + g.ax[2].d * k2 * g.B[2];
+                    const int c3 = ccls[1] + g.ax[1].d * k1 * g.B[1];
+                    const int c4 = static_cast<int>(b_idx * g.ax[0].L) + ccls[0] + g.ax[0].d * k0 * g.B[0];
+#pragma unroll
+                    for (int h = 0; h < C::NH; ++h)
+                        ptx::tma_load_5d(dst + h * C::CHUNK_BYTES, tm, bar, h * 64, h_idx, c2, c3, c4);
+                } else {
+                    const int row = static_cast<int>(cls_row0 + static_cast<long long>((k0 * g.nb[1] + k1) * g.nb[2] + k2) * BV);
+#pragma unroll
+                    for (int h = 0; h < C::NH; ++h) ptx::tma_load_2d(dst + h * C::CHUNK_BYTES, tm, bar, h * 64, row);
+                }
+            };
             ptx::mbar_expect_tx(bar_q, (hasB ? 2 : 1) * C::TILE_BYTES);
             for (int i = 0; i < (hasB ? 2 : 1); ++i) {
                 const int sub = i == 0 ? subA : subB;
@@ -225,12 +248,8 @@ __global__ void __launch_bounds__(384, 1)
                 for (int u = 0; u < KPB; ++u) {
                     // box u of the sub-tile, row-major over the sub-tile's QB box block
                     const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
-                    const int blin = ((sc[0] * g.QB[0] + u0) * g.nb[1] + (sc[1] * g.QB[1] + u1)) * g.nb[2] +
-                                     (sc[2] * g.QB[2] + u2);
-                    const int row = static_cast<int>(cls_row0 + static_cast<long long>(blin) * BV);
-                    for (int h = 0; h < C::NH; ++h)
-                        ptx::tma_load_2d(sQ + i * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, &tmap_q,
-                                         bar_q, h * 64, row);
+                    load_box(&tmap_q, sQ + i * C::TILE_BYTES + u * BV * 128, bar_q, sc[0] * g.QB[0] + u0,
+                             sc[1] * g.QB[1] + u1, sc[2] * g.QB[2] + u2);
                 }
             }
             int it = 0;
@@ -243,12 +262,9 @@ __global__ void __launch_bounds__(384, 1)
                     GT(j, 12 + kind);
                     ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE_BYTES);
                     const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
-                    for (int u = 0; u < KPB; ++u) {
-                        const int row = static_cast<int>(cls_row0 + static_cast<long long>(sb.lin[u]) * BV);
-                        for (int h = 0; h < C::NH; ++h)
-                            ptx::tma_load_2d(sKV + slot * C::TILE_BYTES + h * C::CHUNK_BYTES + u * BV * 128, tm,
-                                             bar_kv_full(slot), h * 64, row);
-                    }
+                    for (int u = 0; u < KPB; ++u)
+                        load_box(tm, sKV + slot * C::TILE_BYTES + u * BV * 128, bar_kv_full(slot), sb.k[u][0], sb.k[u][1],
+                                 sb.k[u][2]);
                 }
             }
         }

@@ -18,6 +18,7 @@ struct AttnParams {
     void* o_perm;           // bf16 permuted O  [BH][C][nbox][box_vol][Dp]
     float* lse_perm;        // fp32 permuted LSE [BH][C][nbox][box_vol]
     float scale_log2;       // softmax scale * log2(e)
+    int direct;             // 1: Q/K/V tensor maps are 5-D maps over the user tensors (no permute pass)
     void* out_nat;          // if non-null: fused inverse permutation, O written to the user layout
     float* lse_nat;         //   and LSE likewise (may be null)
 };

@@ -49,6 +49,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* desc, uint
         : "memory");
 }
 
+// 5-D tiled load (direct, permute-free mode)
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const void* desc, uint32_t bar, int c0, int c1, int c2,
+                                            int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+        : "memory");
+}
+
 // 2-D tile prefetch into L2 (no smem, no completion tracking)
 __device__ __forceinline__ void tma_prefetch_2d(const void* desc, int c0, int c1) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(

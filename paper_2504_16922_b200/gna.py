@@ -20,6 +20,7 @@ GNA_OK, GNA_EINVAL, GNA_EUNSUPPORTED, GNA_ECUDA, GNA_ENOMEM = range(5)
 GNA_DTYPE_BF16 = 0
 GNA_FLAG_SYNC_CHECK = 1
 GNA_FLAG_UNFUSED_EPILOGUE = 2
+GNA_FLAG_PERMUTED = 4
 
 _I3 = ctypes.c_int * 3
 

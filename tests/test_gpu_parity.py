@@ -179,19 +179,24 @@ def test_stages_equal_forward(gna):
     assert torch.equal(out, o2) and torch.equal(lse, l2)
 
 
-def test_fused_epilogue_equals_unfused_path(gna):
-    """The default forward scatters O/LSE from the attention epilogue (fused inverse
-    permutation); GNA_FLAG_UNFUSED_EPILOGUE runs the separate unpermute kernel.
-    Both must agree bit for bit, for every head_dim (D=32 is padded to 64)."""
-    from paper_2504_16922_b200.gna import GNA_FLAG_UNFUSED_EPILOGUE
+@pytest.mark.parametrize("cfg", SMALL, ids=_ids)
+def test_direct_fused_permuted_paths_bitwise(gna, cfg):
+    """Three routes to the same result, bit for bit: the default permute-free path
+    (5-D TMA gathers + epilogue scatter), permute -> attention with the fused
+    epilogue (GNA_FLAG_PERMUTED), and permute -> attention -> unpermute kernel
+    (GNA_FLAG_UNFUSED_EPILOGUE).  Masked / padded keys contribute exact zeros, so
+    the source of padding values (TMA zero fill vs permuted zero rows) is invisible."""
+    from paper_2504_16922_b200.gna import GNA_FLAG_PERMUTED, GNA_FLAG_UNFUSED_EPILOGUE
 
-    for cfg, D in ((SMALL[3], 128), (SMALL[4], 64), (SMALL[1], 32)):
-        q, k, v = (t.cuda() for t in make_qkv(2, cfg["spatial"], 3, D))
-        o1, l1 = gna.forward(q, k, v, cfg["window"], cfg["stride"], cfg["dilation"], cfg["causal"])
-        o2, l2 = gna.forward(q, k, v, cfg["window"], cfg["stride"], cfg["dilation"], cfg["causal"],
-                             flags=GNA_FLAG_UNFUSED_EPILOGUE)
+    for D in (128, 64, 32):
+        q, k, v = (t.cuda() for t in make_qkv(2, cfg["spatial"], 3, D, discriminating=True))
+        res = []
+        for flags in (0, GNA_FLAG_PERMUTED, GNA_FLAG_UNFUSED_EPILOGUE):
+            o, l = gna.forward(q, k, v, cfg["window"], cfg["stride"], cfg["dilation"], cfg["causal"], flags=flags)
+            res.append((o, l))
         torch.cuda.synchronize()
-        assert torch.equal(o1, o2) and torch.equal(l1, l2)
+        for o, l in res[1:]:
+            assert torch.equal(res[0][0], o) and torch.equal(res[0][1], l)
 
 
 def test_work_range_split_is_bitwise(gna):
