@@ -58,11 +58,11 @@ def _load():
             lib.ora_mask.argtypes = [lp, lp, lp, lp, ip, vp]
             lib.ora_count_pairs.argtypes = [lp, lp, lp, lp, ip, vp]
             lib.ora_count_pairs.restype = ctypes.c_longlong
-            lib.ora_forward.argtypes = [vp, vp, vp, vp, vp, ctypes.c_long, ctypes.c_long,
-                                        ctypes.c_long, lp, lp, lp, lp, ip, ctypes.c_double]
+            lib.ora_forward.argtypes = [vp, vp, vp, vp, vp, ctypes.c_long, vp, vp, ctypes.c_long,
+                                        ctypes.c_long, ctypes.c_long, lp, lp, lp, lp, ip, ctypes.c_double]
             lib.ora_forward.restype = ctypes.c_longlong
-            lib.ora_forward_rows.argtypes = [vp, vp, vp, vp, ctypes.c_long, vp, vp,
-                                             ctypes.c_long, ctypes.c_long, ctypes.c_long,
+            lib.ora_forward_rows.argtypes = [vp, vp, vp, vp, vp, ctypes.c_long, vp, ctypes.c_long,
+                                             vp, vp, ctypes.c_long, ctypes.c_long, ctypes.c_long,
                                              lp, lp, lp, lp, ip, ctypes.c_double]
             lib.ora_forward_rows.restype = ctypes.c_longlong
             lib.ora_num_threads.restype = ctypes.c_int
@@ -145,35 +145,48 @@ def count_pairs(p: Params):
     return int(tot), per
 
 
-def forward(q: np.ndarray, k: np.ndarray, v: np.ndarray, p: Params, scale=None):
-    """fp64 GNA forward. q,k,v: float32 [B, *spatial, H, D] (bf16-exact values).
+def _extra(extra_k, extra_v, q):
+    if extra_k is None:
+        return None, None, 0, None
+    ek = np.ascontiguousarray(extra_k, dtype=np.float32)
+    ev = np.ascontiguousarray(extra_v, dtype=np.float32)
+    assert ek.shape == ev.shape and ek.shape[0] == q.shape[0] and ek.shape[2:] == q.shape[-2:]
+    return ek, ev, ek.shape[1], (ek, ev)
+
+
+def forward(q: np.ndarray, k: np.ndarray, v: np.ndarray, p: Params, scale=None, extra_k=None, extra_v=None):
+    """fp64 GNA forward. q,k,v: float32 [B, *spatial, H, D] (bf16-exact values);
+    optional extra (text) keys/values [B, T, H, D] attended by every query.
 
     Returns (out float64 [B,*spatial,H,D], lse float64 [B,*spatial,H])."""
     B, H, D = q.shape[0], q.shape[-2], q.shape[-1]
     q = np.ascontiguousarray(q, dtype=np.float32)
     k = np.ascontiguousarray(k, dtype=np.float32)
     v = np.ascontiguousarray(v, dtype=np.float32)
+    ek, ev, T, _keep = _extra(extra_k, extra_v, q)
     if scale is None or scale <= 0:
         scale = 1.0 / np.sqrt(D)
     out = np.zeros(q.shape, dtype=np.float64)
     lse = np.zeros(q.shape[:-1], dtype=np.float64)
-    _load().ora_forward(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), B, H, D, *p.c(),
-                        float(scale))
+    _load().ora_forward(_ptr(q), _ptr(k), _ptr(v), _ptr(ek) if T else None, _ptr(ev) if T else None, T,
+                        _ptr(out), _ptr(lse), B, H, D, *p.c(), float(scale))
     return out, lse
 
 
-def forward_rows(q, k, v, p: Params, rows: np.ndarray, scale=None):
+def forward_rows(q, k, v, p: Params, rows: np.ndarray, scale=None, extra_k=None, extra_v=None):
     """fp64 forward of selected rows. rows: int64 [R, 3] = (b, token index, h)."""
     B, H, D = q.shape[0], q.shape[-2], q.shape[-1]
     q = np.ascontiguousarray(q, dtype=np.float32)
     k = np.ascontiguousarray(k, dtype=np.float32)
     v = np.ascontiguousarray(v, dtype=np.float32)
+    ek, ev, T, _keep = _extra(extra_k, extra_v, q)
     rows = np.ascontiguousarray(rows, dtype=np.int64)
     if scale is None or scale <= 0:
         scale = 1.0 / np.sqrt(D)
     out = np.zeros((rows.shape[0], D), dtype=np.float64)
     lse = np.zeros(rows.shape[0], dtype=np.float64)
-    pairs = _load().ora_forward_rows(_ptr(q), _ptr(k), _ptr(v), _ptr(rows), rows.shape[0],
+    pairs = _load().ora_forward_rows(_ptr(q), _ptr(k), _ptr(v), _ptr(ek) if T else None,
+                                     _ptr(ev) if T else None, T, _ptr(rows), rows.shape[0],
                                      _ptr(out), _ptr(lse), B, H, D, *p.c(), float(scale))
     return out, lse, int(pairs)
 

@@ -26,6 +26,9 @@
  *                   [max(0, leader-w+1), i'] in class-local index.
  *   attention       P:264-281 §2.2: softmax(scale * q.k) v over the
  *                   neighbourhood; LSE = m + ln(sum exp(z - m)) (natural log).
+ *   extra KV        P:613-618 §3.3 item 5: optional T extra (text) tokens
+ *                   [B][T][H][D] attended densely by every query, in the same
+ *                   softmax as the neighbourhood (S:343-351 reading).
  *   NATTENSim       P:460-584 §3.2: KV tiles visited per Q tile, static
  *                   multi-dimensional tiling, bound = dense / max visited.
  *
@@ -155,6 +158,7 @@ long long ora_count_pairs(const long *L, const long *w, const long *s,
 /* One (b, h, query token n) row.  q,k,v: float [B][N][H][D] (N = L0*L1*L2).
  * out: double[D], *lse: double.  Returns number of attended keys. */
 static long forward_row(const float *q, const float *k, const float *v,
+                        const float *ek, const float *ev, long T,
                         long N, long H, long D, long b, long h, long n,
                         const long *L, const long *w, const long *s, const long *d,
                         const int *causal, double scale, double *out, double *lse,
@@ -172,10 +176,13 @@ static long forward_row(const float *q, const float *k, const float *v,
                 long k0 = c[0] + d[0] * j0, k1 = c[1] + d[1] * j1, k2 = c[2] + d[2] * j2;
                 kbuf[nk++] = (k0 * L[1] + k1) * L[2] + k2;
             }
+    /* extra (text) keys: dense context attended by every query,
+     * layout [B][T][H][D]; they follow the neighbourhood in zbuf */
     const float *qr = q + ((b * N + n) * H + h) * D;
     double m = -INFINITY;
-    for (long i = 0; i < nk; ++i) {
-        const float *kr = k + ((b * N + kbuf[i]) * H + h) * D;
+    for (long i = 0; i < nk + T; ++i) {
+        const float *kr = i < nk ? k + ((b * N + kbuf[i]) * H + h) * D
+                                 : ek + ((b * T + (i - nk)) * H + h) * D;
         double z = 0.0;
         for (long e = 0; e < D; ++e) z += (double)qr[e] * (double)kr[e];
         z *= scale;
@@ -184,26 +191,28 @@ static long forward_row(const float *q, const float *k, const float *v,
     }
     double l = 0.0;
     for (long e = 0; e < D; ++e) out[e] = 0.0;
-    for (long i = 0; i < nk; ++i) {
+    for (long i = 0; i < nk + T; ++i) {
         double p = exp(zbuf[i] - m);
         l += p;
-        const float *vr = v + ((b * N + kbuf[i]) * H + h) * D;
+        const float *vr = i < nk ? v + ((b * N + kbuf[i]) * H + h) * D
+                                 : ev + ((b * T + (i - nk)) * H + h) * D;
         for (long e = 0; e < D; ++e) out[e] += p * (double)vr[e];
     }
     for (long e = 0; e < D; ++e) out[e] /= l;
     *lse = m + log(l);
-    return nk;
+    return nk + T;
 }
 
 /* Full forward: out double [B][N][H][D], lse double [B][N][H].
  * Returns total attended pairs summed over (b, h, query). */
 long long ora_forward(const float *q, const float *k, const float *v,
+                      const float *ek, const float *ev, long T,
                       double *out, double *lse, long B, long H, long D,
                       const long *L, const long *w, const long *s, const long *d,
                       const int *causal, double scale)
 {
     long N = L[0] * L[1] * L[2];
-    long maxk = w[0] * w[1] * w[2];
+    long maxk = w[0] * w[1] * w[2] + T;
     long long total = 0;
     #pragma omp parallel reduction(+ : total)
     {
@@ -212,7 +221,7 @@ long long ora_forward(const float *q, const float *k, const float *v,
         #pragma omp for schedule(dynamic, 16)
         for (long r = 0; r < B * N * H; ++r) {
             long b = r / (N * H), n = (r / H) % N, h = r % H;
-            total += forward_row(q, k, v, N, H, D, b, h, n, L, w, s, d, causal, scale,
+            total += forward_row(q, k, v, ek, ev, T, N, H, D, b, h, n, L, w, s, d, causal, scale,
                                  out + r * D, lse + r, zbuf, kbuf);
         }
         free(zbuf);
@@ -223,12 +232,13 @@ long long ora_forward(const float *q, const float *k, const float *v,
 
 /* Sampled rows: rows[i] = {b, token n, h}.  out double [nrows][D], lse [nrows]. */
 long long ora_forward_rows(const float *q, const float *k, const float *v,
+                           const float *ek, const float *ev, long T,
                            const int64_t *rows, long nrows, double *out, double *lse,
                            long B, long H, long D, const long *L, const long *w,
                            const long *s, const long *d, const int *causal, double scale)
 {
     long N = L[0] * L[1] * L[2];
-    long maxk = w[0] * w[1] * w[2];
+    long maxk = w[0] * w[1] * w[2] + T;
     long long total = 0;
     (void)B;
     #pragma omp parallel reduction(+ : total)
@@ -237,7 +247,7 @@ long long ora_forward_rows(const float *q, const float *k, const float *v,
         long *kbuf = (long *)malloc(sizeof(long) * maxk);
         #pragma omp for schedule(dynamic, 4)
         for (long r = 0; r < nrows; ++r)
-            total += forward_row(q, k, v, N, H, D, rows[3 * r], rows[3 * r + 2], rows[3 * r + 1],
+            total += forward_row(q, k, v, ek, ev, T, N, H, D, rows[3 * r], rows[3 * r + 2], rows[3 * r + 1],
                                  L, w, s, d, causal, scale, out + r * D, lse + r, zbuf, kbuf);
         free(zbuf);
         free(kbuf);

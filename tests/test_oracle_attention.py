@@ -158,3 +158,55 @@ def test_rows_are_convex_combinations():
     vmin = v.min(axis=(1, 2), keepdims=True)
     vmax = v.max(axis=(1, 2), keepdims=True)
     assert (out >= vmin - 1e-12).all() and (out <= vmax + 1e-12).all()
+
+
+def _extra_kv(B, T, H, D, seed):
+    g = torch.Generator("cpu").manual_seed(seed)
+    ek = torch.randn((B, T, H, D), generator=g).to(torch.bfloat16).float().numpy()
+    ev = torch.randn((B, T, H, D), generator=g).to(torch.bfloat16).float().numpy()
+    return ek, ev
+
+
+def test_extra_kv_is_masked_softmax_with_dense_columns():
+    """P:613-618 / SPEC gna_attention(extra_kv): extra (text) keys are attended by every
+    query in the same softmax -- the mask extended by all-true columns."""
+    spatial, w, s = (6, 7), (3, 4), (2, 3)
+    B, H, D, T = 2, 2, 16, 5
+    p, qkv, _, _ = _run_case(spatial, w, s, B=B, H=H, D=D, disc=True)
+    ek, ev = _extra_kv(B, T, H, D, 5)
+    out, lse = O.forward(*qkv, p, extra_k=ek, extra_v=ev)
+    N = p.n_tokens
+    mask = np.concatenate([O.mask(p), np.ones((N, T), dtype=bool)], axis=1)
+    o = out.reshape(B, N, H, D)
+    l = lse.reshape(B, N, H)
+    for b in range(B):
+        for h in range(H):
+            q_, k_, v_ = (_per_head(x, b, h) for x in qkv)
+            k_ = np.concatenate([k_, ek[b, :, h].astype(np.float64)])
+            v_ = np.concatenate([v_, ev[b, :, h].astype(np.float64)])
+            ro, rl = _masked_sdpa(q_, k_, v_, mask, 1.0 / np.sqrt(D))
+            np.testing.assert_allclose(o[b, :, h], ro, atol=1e-12)
+            np.testing.assert_allclose(l[b, :, h], rl, atol=1e-12)
+
+
+def test_extra_kv_equals_lse_merge_of_partials():
+    """attention over (neighbourhood + extra keys) equals the logsumexp merge
+    of the GNA-only partial and a dense attention over the extra keys alone."""
+    spatial, w, s = (5, 4, 6), (3, 2, 3), (1, 2, 3)
+    B, H, D, T = 1, 3, 8, 7
+    p, qkv, out0, lse0 = _run_case(spatial, w, s, B=B, H=H, D=D)
+    ek, ev = _extra_kv(B, T, H, D, 9)
+    out, lse = O.forward(*qkv, p, extra_k=ek, extra_v=ev)
+    N = p.n_tokens
+    qt = torch.from_numpy(qkv[0].reshape(B, N, H, D).astype(np.float64)).permute(0, 2, 1, 3)
+    kt = torch.from_numpy(ek.astype(np.float64)).permute(0, 2, 1, 3)
+    vt = torch.from_numpy(ev.astype(np.float64)).permute(0, 2, 1, 3)
+    z = qt @ kt.transpose(-1, -2) / np.sqrt(D)
+    lse_e = torch.logsumexp(z, -1).permute(0, 2, 1).numpy()
+    out_e = (torch.softmax(z, -1) @ vt).permute(0, 2, 1, 3).numpy()
+    la, lb = lse0.reshape(B, N, H), lse_e
+    m = np.maximum(la, lb)
+    wa, wb = np.exp(la - m), np.exp(lb - m)
+    merged = (wa[..., None] * out0.reshape(B, N, H, D) + wb[..., None] * out_e) / (wa + wb)[..., None]
+    np.testing.assert_allclose(out.reshape(B, N, H, D), merged, atol=1e-12)
+    np.testing.assert_allclose(lse.reshape(B, N, H), m + np.log(wa + wb), atol=1e-12)
