@@ -101,6 +101,12 @@ typedef struct gna_args {
     long long work_begin;   /* Q-tile splitting: global work-item range [begin, end) */
     long long work_end;     /* over (batch*heads) x items; end <= 0 -> all   */
     int flags;
+    /* Extra (text) KV tokens fused into the same kernel:
+     * n_extra keys/values per (batch, head), layout bf16 [B][n_extra][H][D],
+     * attended densely by EVERY query in the same softmax as its GNA
+     * neighbourhood.  0 / NULL = none.  Requires head_dim >= 64. */
+    const void *extra_k, *extra_v;
+    int n_extra;
 } gna_args;
 
 /* Plan summary for a problem (host struct, filled by gna_plan_info). */
@@ -119,8 +125,9 @@ typedef struct gna_plan_info_t {
                                   one unit = 128x128 QK^T + 128x128 PV per head_dim) */
     long long visited_max;  /* max KV boxes visited by one work item */
     long long dense_boxes;  /* KV boxes per class covering all keys */
-    double bound;           /* NATTENSim bound at these tiles: dense / visited_max */
-    long long kept_pairs;   /* sum_q |N(q)| over one (batch, head) */
+    double bound;           /* NATTENSim bound at these tiles: (dense + extra boxes) /
+                               (visited_max + extra boxes) */
+    long long kept_pairs;   /* sum_q (|N(q)| + n_extra) over one (batch, head) */
     size_t workspace_bytes;
 } gna_plan_info_t;
 

@@ -100,6 +100,9 @@ int validate(const gna_args* a, bool need_ptrs) {
         return fail(GNA_EINVAL, "box override volume must be 64 or 128");
     const long long N = static_cast<long long>(a->spatial[0]) * a->spatial[1] * a->spatial[2];
     if (N * a->heads * a->batch > (1LL << 40)) return fail(GNA_EINVAL, "problem too large");
+    if (a->n_extra < 0) return fail(GNA_EINVAL, "n_extra must be >= 0");
+    if (a->n_extra > 0 && a->head_dim < 64) return fail(GNA_EUNSUPPORTED, "extra KV tokens need head_dim >= 64");
+    if (static_cast<long long>(a->n_extra) * a->batch >= (1LL << 31)) return fail(GNA_EINVAL, "n_extra too large");
     if (need_ptrs) {
         const void* ptrs[4] = {a->q, a->k, a->v, a->out};
         const char* names[4] = {"q", "k", "v", "out"};
@@ -108,6 +111,11 @@ int validate(const gna_args* a, bool need_ptrs) {
             if (reinterpret_cast<uintptr_t>(ptrs[i]) % 16) return fail(GNA_EINVAL, std::string(names[i]) + " not 16-byte aligned");
         }
         if (a->lse && reinterpret_cast<uintptr_t>(a->lse) % 4) return fail(GNA_EINVAL, "lse not 4-byte aligned");
+        if (a->n_extra > 0) {
+            if (!a->extra_k || !a->extra_v) return fail(GNA_EINVAL, "extra_k/extra_v NULL with n_extra > 0");
+            if ((reinterpret_cast<uintptr_t>(a->extra_k) | reinterpret_cast<uintptr_t>(a->extra_v)) % 16)
+                return fail(GNA_EINVAL, "extra_k/extra_v not 16-byte aligned");
+        }
     }
     return GNA_OK;
 }
@@ -477,6 +485,22 @@ int make_tmap_direct(CUtensorMap* m, const void* base, const Geometry& g, bool* 
     return GNA_OK;
 }
 
+// 3-D map over extra KV [B][T][H][D]: dims (D, H, B*T), box {64, 1, 128 tokens}.
+int make_tmap_extra(CUtensorMap* m, const void* base, const Geometry& g, int n_extra) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t D = g.D, H = g.heads;
+    cuuint64_t dims[3] = {D, H, static_cast<cuuint64_t>(g.batch) * n_extra};
+    cuuint64_t strides[2] = {D * 2, H * D * 2};
+    cuuint32_t box[3] = {64, 1, 128};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled (extra KV) failed: " + std::to_string(r));
+    return GNA_OK;
+}
+
 int check_device() {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -540,8 +564,18 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
         if ((rc = make_tmap(&tk, c.ws + c.L.k, c.g))) return rc;
         if ((rc = make_tmap(&tv, c.ws + c.L.v, c.g))) return rc;
     }
+    CUtensorMap tek, tev;
+    memset(&tek, 0, sizeof tek);
+    memset(&tev, 0, sizeof tev);
+    if (a->n_extra > 0) {
+        if (!a->extra_k || !a->extra_v) return fail(GNA_EINVAL, "extra_k/extra_v NULL with n_extra > 0");
+        if ((rc = make_tmap_extra(&tek, a->extra_k, c.g, a->n_extra))) return rc;
+        if ((rc = make_tmap_extra(&tev, a->extra_v, c.g, a->n_extra))) return rc;
+    }
     AttnParams p{};
     p.direct = direct ? 1 : 0;
+    p.n_extra = a->n_extra > 0 ? a->n_extra : 0;
+    p.extra_stages = (p.n_extra + 127) / 128;
     p.g = c.g;
     p.items = items;
     p.n_items = static_cast<long long>(c.plan->items.size());
@@ -558,7 +592,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out_nat = fused_out ? a->out : nullptr;
     p.lse_nat = fused_out ? a->lse : nullptr;
-    GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, we - wb, c.st));
+    GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, tek, tev, we - wb, c.st));
     return post_launch(a, c.st, "gna_attn_sm100");
 }
 
@@ -666,6 +700,17 @@ int gna_plan_info(const gna_args* a, gna_plan_info_t* info) {
     auto plan = get_plan(a);
     *info = plan->info;
     info->n_work = info->n_items * a->batch * a->heads;
+    if (a->n_extra > 0) {
+        // extra tokens: dense stages appended to every item; NATTENSim counts
+        // them as always-visited tiles
+        const long long ebox = (a->n_extra + info->box_vol - 1) / info->box_vol;
+        const long long N = static_cast<long long>(a->spatial[0]) * a->spatial[1] * a->spatial[2];
+        info->kept_pairs += N * a->n_extra;
+        info->bound = static_cast<double>(info->dense_boxes + ebox) / static_cast<double>(info->visited_max + ebox);
+        const long long est = (a->n_extra + 127) / 128;
+        info->kv_stages_total += est * info->n_items;
+        info->subtile_stages += est * (info->n_items + info->n_paired);
+    }
     Geometry g = plan->g;
     g.batch = a->batch;
     g.heads = a->heads;

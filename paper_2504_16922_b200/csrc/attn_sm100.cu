@@ -137,7 +137,8 @@ __device__ __forceinline__ u128 box_row_mask(const Geometry& g, const BoxMaskCon
 template <int DP, int BV>
 __global__ void __launch_bounds__(384, 1)
     gna_attn_sm100(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tmap_q,
-                   const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v) {
+                   const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
+                   const __grid_constant__ CUtensorMap tmap_ek, const __grid_constant__ CUtensorMap tmap_ev) {
     using C = Cfg<DP, BV>;
     constexpr int KPB = C::KPB;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -168,8 +169,10 @@ __global__ void __launch_bounds__(384, 1)
     int ext[3];
     for (int a = 0; a < 3; ++a) ext[a] = hi[a] - lo[a];
     const int nkv = ext[0] * ext[1] * ext[2];
-    const int nst = (nkv + KPB - 1) / KPB;
-    if (nst <= 0) return;  // uniform for the CTA: empty item
+    const int nst_gna = (nkv + KPB - 1) / KPB;
+    if (nst_gna <= 0) return;  // uniform for the CTA: empty item
+    // extra (text) KV tokens: dense stages of 128 keys appended after the GNA stages
+    const int nst = nst_gna + p.extra_stages;
 
     // rows of this (bh, class) start here in the permuted buffers
     const long long cls_row0 = ((bh * g.ncls + cls) * static_cast<long long>(g.nbox)) * BV;
@@ -217,6 +220,10 @@ __global__ void __launch_bounds__(384, 1)
             ptx::tma_prefetch_desc(&tmap_q);
             ptx::tma_prefetch_desc(&tmap_k);
             ptx::tma_prefetch_desc(&tmap_v);
+            if (p.n_extra > 0) {
+                ptx::tma_prefetch_desc(&tmap_ek);
+                ptx::tma_prefetch_desc(&tmap_ev);
+            }
             // One box of 64/128 token rows, both D halves.  Permuted mode: a contiguous row
             // range of the permuted tensor (2-D map).  Direct mode (permute-free, SURVEY
             // NEXT-2): a 5-D box {64 cols, 1 head, B2, B1, B0 tokens} of the user's
@@ -255,16 +262,27 @@ __global__ void __launch_bounds__(384, 1)
             int it = 0;
             StageBoxes sb;
             for (int j = 0; j < nst; ++j) {
-                decode_stage(g, lo, ext, nkv, j, KPB, sb);
+                if (j < nst_gna) decode_stage(g, lo, ext, nkv, j, KPB, sb);
                 for (int kind = 0; kind < 2; ++kind, ++it) {
                     const int slot = it % C::NS;
                     ptx::mbar_wait(bar_kv_empty(slot), ((it / C::NS) & 1) ^ 1);
                     GT(j, 12 + kind);
                     ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE_BYTES);
-                    const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
-                    for (int u = 0; u < KPB; ++u)
-                        load_box(tm, sKV + slot * C::TILE_BYTES + u * BV * 128, bar_kv_full(slot), sb.k[u][0], sb.k[u][1],
-                                 sb.k[u][2]);
+                    if (j < nst_gna) {
+                        const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
+                        for (int u = 0; u < KPB; ++u)
+                            load_box(tm, sKV + slot * C::TILE_BYTES + u * BV * 128, bar_kv_full(slot), sb.k[u][0],
+                                     sb.k[u][1], sb.k[u][2]);
+                    } else {
+                        // 128 extra tokens [b*T + e*128, +128) of head h; rows past T belong to the
+                        // next batch or are zero-filled, and are masked by the softmax
+                        const CUtensorMap* tm = kind == 0 ? &tmap_ek : &tmap_ev;
+                        const int row = static_cast<int>(b_idx * p.n_extra) + (j - nst_gna) * 128;
+#pragma unroll
+                        for (int h = 0; h < C::NH; ++h)
+                            ptx::tma_load_3d(sKV + slot * C::TILE_BYTES + h * C::CHUNK_BYTES, tm, bar_kv_full(slot), h * 64,
+                                             h_idx, row);
+                    }
                 }
             }
         }
@@ -389,7 +407,8 @@ __global__ void __launch_bounds__(384, 1)
         float l_run = 0.f;
         StageBoxes sb;
         for (int j = 0; j < nst; ++j) {
-            decode_stage(g, lo, ext, nkv, j, KPB, sb);
+            const bool extra_stage = j >= nst_gna;
+            decode_stage(g, lo, ext, nkv, extra_stage ? 0 : j, KPB, sb);
             // per-row coverage of every key of the stage; padded rows never mask
             bool row_full = true;
             int rlo[KPB][3], rhi[KPB][3];
@@ -403,7 +422,10 @@ __global__ void __launch_bounds__(384, 1)
                     row_full = row_full && rlo[u][a] <= 0 && rhi[u][a] >= g.B[a];
                 }
             }
-            const bool warp_full = __all_sync(0xffffffffu, row_full || !valid);
+            // extra stages: dense, only the tail past n_extra is masked (uniform)
+            const int extra_left = p.n_extra - (j - nst_gna) * 128;
+            const bool warp_full =
+                extra_stage ? extra_left >= 128 : __all_sync(0xffffffffu, row_full || !valid);
 
             ptx::mbar_wait(bar_s, j & 1);
             if (r == 0) GT(j, 4 * i + 0);
@@ -420,8 +442,13 @@ __global__ void __launch_bounds__(384, 1)
             if (r == 0) GT(j, 4 * i + 1);
             if (!warp_full) {
                 // 128-bit row mask of the stage (1 or 2 boxes), then one select per element
-                u128 m = box_row_mask(g, mconst, rlo[0], rhi[0]);
-                if (KPB == 2) m |= box_row_mask(g, mconst, rlo[KPB - 1], rhi[KPB - 1]) << 64;
+                u128 m;
+                if (extra_stage) {
+                    m = bits_below(extra_left);  // keys [0, n_extra - e*128) of the extra stage
+                } else {
+                    m = box_row_mask(g, mconst, rlo[0], rhi[0]);
+                    if (KPB == 2) m |= box_row_mask(g, mconst, rlo[KPB - 1], rhi[KPB - 1]) << 64;
+                }
                 const uint32_t mw[4] = {static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32),
                                         static_cast<uint32_t>(m >> 64), static_cast<uint32_t>(m >> 96)};
 #pragma unroll
@@ -542,7 +569,8 @@ __global__ void __launch_bounds__(384, 1)
 
 template <int DP, int BV>
 static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                            const CUtensorMap& tv, long long n_ctas, cudaStream_t stream) {
+                            const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
+                            cudaStream_t stream) {
     using C = Cfg<DP, BV>;
     static bool configured = false;
     if (!configured) {
@@ -552,17 +580,18 @@ static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CU
         configured = true;
     }
     if (n_ctas <= 0) return cudaSuccess;
-    gna_attn_sm100<DP, BV><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv);
+    gna_attn_sm100<DP, BV><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
     return cudaGetLastError();
 }
 
 cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, long long n_ctas, cudaStream_t stream) {
+                             const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
+                             cudaStream_t stream) {
     const int dp = p.g.Dp, bv = p.g.box_vol;
-    if (dp == 128 && bv == 128) return launch_t<128, 128>(p, tq, tk, tv, n_ctas, stream);
-    if (dp == 128 && bv == 64) return launch_t<128, 64>(p, tq, tk, tv, n_ctas, stream);
-    if (dp == 64 && bv == 128) return launch_t<64, 128>(p, tq, tk, tv, n_ctas, stream);
-    if (dp == 64 && bv == 64) return launch_t<64, 64>(p, tq, tk, tv, n_ctas, stream);
+    if (dp == 128 && bv == 128) return launch_t<128, 128>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+    if (dp == 128 && bv == 64) return launch_t<128, 64>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+    if (dp == 64 && bv == 128) return launch_t<64, 128>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+    if (dp == 64 && bv == 64) return launch_t<64, 64>(p, tq, tk, tv, tek, tev, n_ctas, stream);
     return cudaErrorInvalidValue;
 }
 

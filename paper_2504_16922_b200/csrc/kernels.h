@@ -19,6 +19,8 @@ struct AttnParams {
     float* lse_perm;        // fp32 permuted LSE [BH][C][nbox][box_vol]
     float scale_log2;       // softmax scale * log2(e)
     int direct;             // 1: Q/K/V tensor maps are 5-D maps over the user tensors (no permute pass)
+    int n_extra;            // extra (text) KV tokens per (batch, head), appended as dense stages
+    int extra_stages;       // ceil(n_extra / 128)
     void* out_nat;          // if non-null: fused inverse permutation, O written to the user layout
     float* lse_nat;         //   and LSE likewise (may be null)
 };
@@ -29,7 +31,8 @@ inline long long perm_rows(const Geometry& g) {
 }
 
 cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                             const CUtensorMap& tv, long long n_ctas, cudaStream_t stream);
+                             const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
+                             cudaStream_t stream);
 
 // q/k/v natural [B][s0][s1][s2][H][D] -> permuted [BH][C][nbox][box_vol][Dp]
 cudaError_t launch_permute_qkv(const Geometry& g, const void* q, const void* k, const void* v, void* qp,

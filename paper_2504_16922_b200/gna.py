@@ -35,6 +35,7 @@ class GnaArgs(ctypes.Structure):
         ("stream", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
         ("box", _I3), ("work_begin", ctypes.c_longlong), ("work_end", ctypes.c_longlong),
         ("flags", ctypes.c_int),
+        ("extra_k", ctypes.c_void_p), ("extra_v", ctypes.c_void_p), ("n_extra", ctypes.c_int),
     ]
 
 
@@ -97,7 +98,8 @@ def _pad3(x, fill):
 
 def make_args(batch, heads, head_dim, spatial, window, stride=None, dilation=None, causal=None,
               scale=0.0, q=None, k=None, v=None, out=None, lse=None, stream=None, box=None,
-              work_range=None, workspace=None, workspace_bytes=0, flags=0) -> GnaArgs:
+              work_range=None, workspace=None, workspace_bytes=0, flags=0, extra_k=None, extra_v=None,
+              n_extra=0) -> GnaArgs:
     n = len(spatial)
     a = GnaArgs()
     a.q, a.k, a.v, a.out, a.lse = q, k, v, out, lse
@@ -115,11 +117,12 @@ def make_args(batch, heads, head_dim, spatial, window, stride=None, dilation=Non
     a.box = _I3(*(_pad3(box, 1) if box else [0, 0, 0]))
     a.work_begin, a.work_end = (work_range if work_range is not None else (0, 0))
     a.flags = int(flags)
+    a.extra_k, a.extra_v, a.n_extra = extra_k, extra_v, int(n_extra)
     return a
 
 
 def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,
-                 workspace=None):
+                 workspace=None, extra_k=None, extra_v=None):
     import torch
 
     for name, t in (("q", q), ("k", k), ("v", v), ("out", out)):
@@ -140,15 +143,28 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
         if not workspace.is_cuda or not workspace.is_contiguous():
             raise GnaError("workspace must be a contiguous CUDA tensor")
         ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    ek = ev = None
+    n_extra = 0
+    if extra_k is not None:
+        for name, t in (("extra_k", extra_k), ("extra_v", extra_v)):
+            if t is None or not t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
+                raise GnaError(f"{name} must be a contiguous CUDA bfloat16 tensor [B, T, H, D]")
+        if extra_k.shape != extra_v.shape or extra_k.dim() != 4 or extra_k.shape[0] != batch or \
+                tuple(extra_k.shape[2:]) != (heads, head_dim):
+            raise GnaError("extra_k/extra_v must be [B, T, H, D] matching q")
+        ek, ev, n_extra = extra_k.data_ptr(), extra_v.data_ptr(), extra_k.shape[1]
     return make_args(batch, heads, head_dim, spatial, window, stride, dilation, causal, scale,
                      q=q.data_ptr(), k=k.data_ptr(), v=v.data_ptr(), out=out.data_ptr(),
                      lse=(lse.data_ptr() if lse is not None else None), stream=stream, box=box,
-                     work_range=work_range, flags=flags, workspace=ws_ptr, workspace_bytes=ws_bytes)
+                     work_range=work_range, flags=flags, workspace=ws_ptr, workspace_bytes=ws_bytes,
+                     extra_k=ek, extra_v=ev, n_extra=n_extra)
 
 
 def forward(q, k, v, window, stride=None, dilation=None, causal=None, scale=None, out=None, lse=None,
-            box=None, work_range=None, stream=None, return_lse=True, flags=0, workspace=None):
-    """GNA forward on CUDA bf16 tensors [B, *spatial, H, D] (heads-last).
+            box=None, work_range=None, stream=None, return_lse=True, flags=0, workspace=None, extra_k=None,
+            extra_v=None):
+    """GNA forward on CUDA bf16 tensors [B, *spatial, H, D] (heads-last); optional extra
+    (text) keys/values [B, T, H, D] attended densely by every query.
 
     Returns (out, lse) -- lse fp32 [B, *spatial, H] (natural log)."""
     import torch
@@ -158,18 +174,18 @@ def forward(q, k, v, window, stride=None, dilation=None, causal=None, scale=None
     if lse is None and return_lse:
         lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
     a = _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,
-                     workspace)
+                     workspace, extra_k, extra_v)
     with torch.cuda.device(q.device):
         _check(load().gna_forward_ex(ctypes.byref(a)))
     return out, lse
 
 
 def _stage(fn_name, q, k, v, out, lse, window, stride, dilation, causal, scale, box, stream, flags,
-           workspace=None, work_range=None):
+           workspace=None, work_range=None, extra_k=None, extra_v=None):
     import torch
 
     a = _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,
-                     workspace)
+                     workspace, extra_k, extra_v)
     with torch.cuda.device(q.device):
         _check(getattr(load(), fn_name)(ctypes.byref(a)))
 
@@ -179,9 +195,9 @@ def permute(q, k, v, out, window, stride=None, dilation=None, causal=None, box=N
 
 
 def attention_permuted(q, k, v, out, window, stride=None, dilation=None, causal=None, scale=None, box=None,
-                       stream=None, workspace=None, work_range=None):
+                       stream=None, workspace=None, work_range=None, extra_k=None, extra_v=None):
     _stage("gna_attention_permuted", q, k, v, out, None, window, stride, dilation, causal, scale, box, stream, 0,
-           workspace, work_range)
+           workspace, work_range, extra_k, extra_v)
 
 
 def unpermute(q, k, v, out, lse, window, stride=None, dilation=None, causal=None, box=None, stream=None,
@@ -189,8 +205,9 @@ def unpermute(q, k, v, out, lse, window, stride=None, dilation=None, causal=None
     _stage("gna_unpermute", q, k, v, out, lse, window, stride, dilation, causal, None, box, stream, 0, workspace)
 
 
-def plan_info(batch, heads, head_dim, spatial, window, stride=None, dilation=None, causal=None, box=None) -> dict:
-    a = make_args(batch, heads, head_dim, spatial, window, stride, dilation, causal, box=box)
+def plan_info(batch, heads, head_dim, spatial, window, stride=None, dilation=None, causal=None, box=None,
+              n_extra=0) -> dict:
+    a = make_args(batch, heads, head_dim, spatial, window, stride, dilation, causal, box=box, n_extra=n_extra)
     info = GnaPlanInfo()
     _check(load().gna_plan_info(ctypes.byref(a), ctypes.byref(info)))
     d = {f: getattr(info, f) for f, _ in GnaPlanInfo._fields_}

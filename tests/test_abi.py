@@ -135,3 +135,24 @@ def test_worklist_covers_every_subtile_once(gna):
             Lc = O.class_extents(O.Params(f["spatial"], f["window"], f["stride"], f["dilation"], f["causal"]), cls)
             n_nonempty = int(np.prod([-(-Lc[a] // q_sub[a]) for a in range(3)]))
             assert sum(1 for (c, _s) in seen if c == cls) == n_nonempty, name
+
+
+def test_plan_info_extra_tokens(gna):
+    """Extra KV tokens: kept pairs grow by N*T; the NATTENSim bound counts the extra
+    tiles as always visited: (dense + e) / (visited_max + e)."""
+    w = WORKLOADS["x1_hunyuan_s16"]
+    f = w.full()
+    base = gna.plan_info(1, 1, 128, **f)
+    ext = gna.plan_info(1, 1, 128, **f, n_extra=256)
+    e = -(-256 // base["box_vol"])
+    assert ext["kept_pairs"] == base["kept_pairs"] + w.n_tokens * 256
+    assert ext["bound"] == pytest.approx((base["dense_boxes"] + e) / (base["visited_max"] + e))
+
+
+def test_extra_tokens_validation(gna):
+    from paper_2504_16922_b200.gna import GnaError
+
+    with pytest.raises(GnaError, match="head_dim >= 64"):
+        gna.plan_info(1, 1, 32, (64,), (8,), n_extra=4)
+    with pytest.raises(GnaError, match="n_extra"):
+        gna.plan_info(1, 1, 64, (64,), (8,), n_extra=-1)

@@ -241,3 +241,33 @@ def test_invalid_args_launch_nothing(gna):
     q = torch.zeros(1, 16, 1, 64, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(GnaError, match="holes"):
         gna.forward(q, q, q, (4,), (5,))
+
+
+def _extra(B, T, H, D, seed=77):
+    g = torch.Generator("cpu").manual_seed(seed)
+    ek = torch.randn((B, T, H, D), generator=g).to(torch.bfloat16)
+    ev = (torch.rand((B, T, H, D), generator=g) * 2 - 1).to(torch.bfloat16)
+    return ek, ev
+
+
+@pytest.mark.parametrize("T", [1, 77, 128, 300])
+@pytest.mark.parametrize("cfg", [SMALL[2], SMALL[4], SMALL[6]], ids=_ids)
+def test_extra_kv_tokens(gna, cfg, T):
+    """NEXT-1: extra text tokens attended by every query, fused into the same
+    kernel as dense stages; both the permute-free and the permuted path vs the oracle."""
+    from paper_2504_16922_b200.gna import GNA_FLAG_PERMUTED
+
+    B, H = 2, 2
+    for D in (128, 64):
+        q, k, v = make_qkv(B, cfg["spatial"], H, D, discriminating=True)
+        ek, ev = _extra(B, T, H, D)
+        ro, rl = O.forward(as_f32_numpy(q), as_f32_numpy(k), as_f32_numpy(v), O.Params(**cfg),
+                           extra_k=as_f32_numpy(ek), extra_v=as_f32_numpy(ev))
+        outs = []
+        for flags in (0, GNA_FLAG_PERMUTED):
+            o, l = gna.forward(q.cuda(), k.cuda(), v.cuda(), cfg["window"], cfg["stride"], cfg["dilation"],
+                               cfg["causal"], flags=flags, extra_k=ek.cuda(), extra_v=ev.cuda())
+            torch.cuda.synchronize()
+            outs.append((o, l))
+            _assert_close(o.float().cpu().numpy(), ro, l.cpu().numpy(), rl)
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
