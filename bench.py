@@ -321,7 +321,10 @@ def run_ours(args, ws, rank, local):
     ms_per_step = total_ms / args.steps
     value = ws * eff_flops / (ms_per_step * 1e-3) / 1e12
     e2e_value = ws * eff_flops / (e2e_total / args.steps * 1e-3) / 1e12
-    achieved = eff_flops / (att_ms * 1e-3) / 1e12
+    # dominant kernel: the one-kernel direct route when it applies (the step IS that launch),
+    # else the attention kernel of the permuted pipeline
+    kernel_ms = ms_per_step if direct else att_ms
+    achieved = eff_flops / (kernel_ms * 1e-3) / 1e12
     mma_flops = 4.0 * info["padded_head_dim"] * 128 * 128 * info["subtile_stages"] * B * H  # issued (both GEMMs)
     n_tok = w.n_tokens
     nat_bytes = B * n_tok * H * D * 2
@@ -350,10 +353,12 @@ def run_ours(args, ws, rank, local):
         "dense_effective_tflops": 4.0 * D * n_tok * n_tok * B * H / (statistics.mean(dense_ms) * 1e-3) / 1e12,
         "permute_gbs": perm_bytes / (statistics.mean(stage["permute"]) * 1e-3) / 1e9,
         "unpermute_gbs": unperm_bytes / (statistics.mean(stage["unpermute"]) * 1e-3) / 1e9,
-        "mma_issued_tflops": mma_flops / (att_ms * 1e-3) / 1e12,
+        "mma_issued_tflops": mma_flops / (kernel_ms * 1e-3) / 1e12,
+        "permuted_pipeline_attention_tflops": eff_flops / (att_ms * 1e-3) / 1e12,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
                      "frac": achieved / peak_burst, "traffic": _traffic_from_profiles(w.name),
-                     "kernel": "gna_attn_sm100", "peak_kind": f"{peak_kind} bf16 burst",
+                     "kernel": "gna_attn_sm100 (direct, one kernel per step)" if direct else "gna_attn_sm100",
+                     "peak_kind": f"{peak_kind} bf16 burst",
                      "frac_of_sustained": achieved / peak_sus},
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": 3 * nat_bytes,
                 "d2h_bytes_per_step": nat_bytes + B * n_tok * H * 4},

@@ -271,3 +271,33 @@ def test_extra_kv_tokens(gna, cfg, T):
             outs.append((o, l))
             _assert_close(o.float().cpu().numpy(), ro, l.cpu().numpy(), rl)
         assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("name", ["s1_sweep1d", "s2_sweep2d", "s2c_sweep2d_causal", "s3_sweep3d"])
+def test_sweep_configs_sampled(gna, name):
+    """configs[4]: the batch-8 sweep rows with dilation 2 and per-axis causal masks, at full
+    size through the default launch path, on sampled rows (every batch, class corners)."""
+    w = WORKLOADS[name]
+    f = w.full()
+    (q, k, v), o, l = _run(gna, f, w.batch, w.heads, w.head_dim, True)
+    L = list(w.spatial) + [1] * (3 - len(w.spatial))
+    corners = [0, 1, w.n_tokens - 1, w.n_tokens - 2, (L[0] // 2) * L[1] * L[2] + 1]
+    rows = sample_rows(w.batch, w.spatial, w.heads, 48, extra_tokens=corners)
+    ro, rl, _ = O.forward_rows(as_f32_numpy(q), as_f32_numpy(k), as_f32_numpy(v), O.Params(**f), rows)
+    oo = o.reshape(w.batch, -1, w.heads, w.head_dim)[rows[:, 0], rows[:, 1], rows[:, 2]]
+    ll = l.reshape(w.batch, -1, w.heads)[rows[:, 0], rows[:, 1], rows[:, 2]]
+    _assert_close(oo, ro, ll, rl)
+
+
+@pytest.mark.parametrize("cfg", [
+    _cfg((1,), (1,), (1,)),                       # a single token: attends itself only
+    _cfg((3, 1, 2), (1, 1, 1), (1, 1, 1)),        # window 1: O = V, LSE = logit
+    _cfg((5,), (5,), (5,), causal=(True,)),       # one causal block smaller than any box
+    _cfg((2, 3, 130), (2, 3, 7), (1, 3, 7)),      # 3-D with a long last axis (boxes beyond 128)
+    _cfg((129,), (129,), (1,)),                   # dense, one key past a 128 box
+], ids=_ids)
+def test_degenerate_shapes(gna, cfg):
+    B, H, D = 3, 2, 64
+    (q, k, v), o, l = _run(gna, cfg, B, H, D, True)
+    ro, rl = O.forward(as_f32_numpy(q), as_f32_numpy(k), as_f32_numpy(v), O.Params(**cfg))
+    _assert_close(o, ro, l, rl)
