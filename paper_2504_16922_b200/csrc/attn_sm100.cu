@@ -52,6 +52,15 @@ __device__ unsigned long long g_gna_trace[GNA_TRACE_CTAS][GNA_TRACE_STAGES][16];
     } while (0)
 #endif
 
+// Compile-time variants for A/B measurements (scripts/ab.py); defaults are the
+// measured best.
+#ifndef GNA_POLY_EVERY
+#define GNA_POLY_EVERY 4  // 1 exp pair in GNA_POLY_EVERY on the FMA pipe (0 = all MUFU)
+#endif
+#ifndef GNA_PHALF
+#define GNA_PHALF 0  // 1: hand P to the MMA in two halves (PV of keys 0-63 starts earlier)
+#endif
+
 namespace gna {
 
 namespace {
@@ -187,7 +196,8 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t bar_s_full0 = bar0 + 8u * (1 + 2 * C::NS);
     const uint32_t bar_p_full0 = bar_s_full0 + 16;
     const uint32_t bar_o_full = bar_p_full0 + 16;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 8 * (1 + 2 * C::NS) + 40);
+    const uint32_t bar_ph0 = bar_o_full + 8;  // [2] first half of P ready (GNA_PHALF)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 8 * (1 + 2 * C::NS) + 64);
 
     if (threadIdx.x == 0) {
         GT(0, 15);
@@ -201,6 +211,8 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_init(bar_p_full0, 128);
         ptx::mbar_init(bar_p_full0 + 8, 128);
         ptx::mbar_init(bar_o_full, 1);
+        ptx::mbar_init(bar_ph0, 128);
+        ptx::mbar_init(bar_ph0 + 8, 128);
         ptx::fence_mbar_init();
     }
     if (warp == 8) {
@@ -303,10 +315,10 @@ __global__ void __launch_bounds__(384, 1)
                                 ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
                 }
             };
-            auto issue_pv = [&](int i, int slot, bool acc) {
+            auto issue_pv = [&](int i, int slot, bool acc, int k0 = 0, int k1 = 8) {
                 const uint32_t vb = sKV + slot * C::TILE_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
+                for (int kk = k0; kk < k1; ++kk) {
                     ptx::mma_ts(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + kk * 8,
                                 ptx::smem_desc_sw128(vb + kk * 2048, C::CHUNK_BYTES, 1024), IDESC_PV,
                                 (acc || kk > 0) ? 1u : 0u);
@@ -331,10 +343,20 @@ __global__ void __launch_bounds__(384, 1)
                 GT(j, 8);
                 ++it;
                 const bool has_next = j + 1 < nst;
+#if GNA_PHALF
+                ptx::mbar_wait(bar_ph0, j & 1);
+                ptx::tc_fence_after();
+                issue_pv(0, slotV, j > 0, 0, 4);
+                ptx::mbar_wait(bar_p_full0, j & 1);
+                GT(j, 9);
+                ptx::tc_fence_after();
+                issue_pv(0, slotV, true, 4, 8);
+#else
                 ptx::mbar_wait(bar_p_full0, j & 1);
                 GT(j, 9);
                 ptx::tc_fence_after();
                 issue_pv(0, slotV, j > 0);
+#endif
                 if (has_next) {
                     slotK = it % C::NS;
                     ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
@@ -345,10 +367,20 @@ __global__ void __launch_bounds__(384, 1)
                     ptx::mma_commit(bar_s_full0);
                 }
                 if (hasB) {
+#if GNA_PHALF
+                    ptx::mbar_wait(bar_ph0 + 8, j & 1);
+                    ptx::tc_fence_after();
+                    issue_pv(1, slotV, j > 0, 0, 4);
+                    ptx::mbar_wait(bar_p_full0 + 8, j & 1);
+                    GT(j, 10);
+                    ptx::tc_fence_after();
+                    issue_pv(1, slotV, true, 4, 8);
+#else
                     ptx::mbar_wait(bar_p_full0 + 8, j & 1);
                     GT(j, 10);
                     ptx::tc_fence_after();
                     issue_pv(1, slotV, j > 0);
+#endif
                 }
                 ptx::mma_commit(bar_kv_empty(slotV));
                 if (has_next) {
@@ -491,7 +523,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int pi = 0; pi < 64; ++pi) {
                 float x0, x1, y0, y1;
                 ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
-                if ((pi & 3) == 3) {
+                if (GNA_POLY_EVERY > 0 && (pi % (GNA_POLY_EVERY > 0 ? GNA_POLY_EVERY : 1)) == GNA_POLY_EVERY - 1) {
                     ptx::ex2_poly2(y0, y1, x0, x1);
                 } else {
                     y0 = ptx::ex2(x0);
@@ -500,9 +532,19 @@ __global__ void __launch_bounds__(384, 1)
                 if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
                 else ptx::fadd2(la0, la1, la0, la1, y0, y1);
                 pk[pi] = ptx::pack_bf16x2(y0, y1);
+#if GNA_PHALF
+                if (pi == 31) {  // keys 0-63 of P are final: let the MMA start PV on them
+                    ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(bar_ph0 + 8 * i);
+                }
+#endif
             }
             l_run += (la0 + la1) + (lb0 + lb1);
+#if !GNA_PHALF
             ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
+#endif
             ptx::tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pk[32]));
             ptx::tmem_wait_st();
             if (r == 0) GT(j, 4 * i + 3);
