@@ -55,10 +55,14 @@ __device__ unsigned long long g_gna_trace[GNA_TRACE_CTAS][GNA_TRACE_STAGES][16];
 // Compile-time variants for A/B measurements (scripts/ab.py); defaults are the
 // measured best.
 #ifndef GNA_POLY_EVERY
-#define GNA_POLY_EVERY 4  // 1 exp pair in GNA_POLY_EVERY on the FMA pipe (0 = all MUFU)
+#define GNA_POLY_EVERY 8  // 1 exp pair in GNA_POLY_EVERY on the FMA pipe (0 = all MUFU)
 #endif
-#ifndef GNA_PHALF
-#define GNA_PHALF 0  // 1: hand P to the MMA in two halves (PV of keys 0-63 starts earlier)
+#ifndef GNA_NS128
+#define GNA_NS128 4  // K/V ring slots of 32 KB at head_dim 128
+#endif
+#ifndef GNA_PSPLIT
+#define GNA_PSPLIT 2  // P is handed to the MMA in GNA_PSPLIT chunks (1, 2 or 4): the PV of the
+                      // first keys starts while the softmax still computes the last ones
 #endif
 
 namespace gna {
@@ -70,7 +74,7 @@ struct Cfg {
     static constexpr int NH = DP / 64;               // 128-byte column chunks ("halves")
     static constexpr int CHUNK_BYTES = 128 * 128;    // 128 rows x 128 B, one SW128 chunk
     static constexpr int TILE_BYTES = NH * CHUNK_BYTES;  // 128 rows x DP bf16
-    static constexpr int NS = DP == 128 ? 4 : 8;     // KV ring slots (K and V share it)
+    static constexpr int NS = DP == 128 ? GNA_NS128 : 8;  // KV ring slots (K and V share it)
     static constexpr int KPB = 128 / BV;             // boxes per 128-row tile
     static constexpr int Q_OFF = 0;
     static constexpr int KV_OFF = 2 * TILE_BYTES;
@@ -196,8 +200,8 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t bar_s_full0 = bar0 + 8u * (1 + 2 * C::NS);
     const uint32_t bar_p_full0 = bar_s_full0 + 16;
     const uint32_t bar_o_full = bar_p_full0 + 16;
-    const uint32_t bar_ph0 = bar_o_full + 8;  // [2] first half of P ready (GNA_PHALF)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 8 * (1 + 2 * C::NS) + 64);
+    const uint32_t bar_pc0 = bar_o_full + 8;  // [2][3] P chunk c of sub-tile i ready (GNA_PSPLIT)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 8 * (1 + 2 * C::NS) + 96);
 
     if (threadIdx.x == 0) {
         GT(0, 15);
@@ -211,8 +215,7 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_init(bar_p_full0, 128);
         ptx::mbar_init(bar_p_full0 + 8, 128);
         ptx::mbar_init(bar_o_full, 1);
-        ptx::mbar_init(bar_ph0, 128);
-        ptx::mbar_init(bar_ph0 + 8, 128);
+        for (int c = 0; c < 6; ++c) ptx::mbar_init(bar_pc0 + 8 * c, 128);
         ptx::fence_mbar_init();
     }
     if (warp == 8) {
@@ -343,20 +346,16 @@ __global__ void __launch_bounds__(384, 1)
                 GT(j, 8);
                 ++it;
                 const bool has_next = j + 1 < nst;
-#if GNA_PHALF
-                ptx::mbar_wait(bar_ph0, j & 1);
-                ptx::tc_fence_after();
-                issue_pv(0, slotV, j > 0, 0, 4);
+#pragma unroll
+                for (int c = 0; c < GNA_PSPLIT - 1; ++c) {
+                    ptx::mbar_wait(bar_pc0 + 8 * c, j & 1);
+                    ptx::tc_fence_after();
+                    issue_pv(0, slotV, j > 0 || c > 0, c * 8 / GNA_PSPLIT, (c + 1) * 8 / GNA_PSPLIT);
+                }
                 ptx::mbar_wait(bar_p_full0, j & 1);
                 GT(j, 9);
                 ptx::tc_fence_after();
-                issue_pv(0, slotV, true, 4, 8);
-#else
-                ptx::mbar_wait(bar_p_full0, j & 1);
-                GT(j, 9);
-                ptx::tc_fence_after();
-                issue_pv(0, slotV, j > 0);
-#endif
+                issue_pv(0, slotV, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * 8 / GNA_PSPLIT, 8);
                 if (has_next) {
                     slotK = it % C::NS;
                     ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
@@ -367,20 +366,16 @@ __global__ void __launch_bounds__(384, 1)
                     ptx::mma_commit(bar_s_full0);
                 }
                 if (hasB) {
-#if GNA_PHALF
-                    ptx::mbar_wait(bar_ph0 + 8, j & 1);
-                    ptx::tc_fence_after();
-                    issue_pv(1, slotV, j > 0, 0, 4);
+#pragma unroll
+                    for (int c = 0; c < GNA_PSPLIT - 1; ++c) {
+                        ptx::mbar_wait(bar_pc0 + 8 * (3 + c), j & 1);
+                        ptx::tc_fence_after();
+                        issue_pv(1, slotV, j > 0 || c > 0, c * 8 / GNA_PSPLIT, (c + 1) * 8 / GNA_PSPLIT);
+                    }
                     ptx::mbar_wait(bar_p_full0 + 8, j & 1);
                     GT(j, 10);
                     ptx::tc_fence_after();
-                    issue_pv(1, slotV, true, 4, 8);
-#else
-                    ptx::mbar_wait(bar_p_full0 + 8, j & 1);
-                    GT(j, 10);
-                    ptx::tc_fence_after();
-                    issue_pv(1, slotV, j > 0);
-#endif
+                    issue_pv(1, slotV, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * 8 / GNA_PSPLIT, 8);
                 }
                 ptx::mma_commit(bar_kv_empty(slotV));
                 if (has_next) {
@@ -532,20 +527,25 @@ __global__ void __launch_bounds__(384, 1)
                 if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
                 else ptx::fadd2(la0, la1, la0, la1, y0, y1);
                 pk[pi] = ptx::pack_bf16x2(y0, y1);
-#if GNA_PHALF
-                if (pi == 31) {  // keys 0-63 of P are final: let the MMA start PV on them
-                    ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
-                    ptx::tmem_wait_st();
-                    ptx::tc_fence_before();
-                    ptx::mbar_arrive(bar_ph0 + 8 * i);
+                constexpr int CH = 64 / GNA_PSPLIT;  // packed P columns per chunk
+                if (pi % CH == CH - 1) {
+                    // P columns of this chunk (keys [2*(pi+1-CH), 2*(pi+1))) are final: store them and,
+                    // except for the last chunk, let the MMA start the PV on them right away
+                    const int c0 = pi + 1 - CH;
+                    if (CH == 32) ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
+                    else if (CH == 16) ptx::tmem_st16(tS + c0, &pk[c0]);
+                    else {
+                        ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
+                        ptx::tmem_st32(tS + c0 + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0 + 32]));
+                    }
+                    if (pi < 63) {
+                        ptx::tmem_wait_st();
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(bar_pc0 + 8 * (3 * i + pi / CH));
+                    }
                 }
-#endif
             }
             l_run += (la0 + la1) + (lb0 + lb1);
-#if !GNA_PHALF
-            ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
-#endif
-            ptx::tmem_st32(tS + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pk[32]));
             ptx::tmem_wait_st();
             if (r == 0) GT(j, 4 * i + 3);
             ptx::tc_fence_before();
