@@ -131,6 +131,52 @@ typedef struct gna_plan_info_t {
     size_t workspace_bytes;
 } gna_plan_info_t;
 
+/* ------------------------------------------------------------------------
+ * NATTENSim (§3.2): analytical tile simulator, host only.
+ * Counts the KV tiles each Q tile visits under a kernel design -- static
+ * multi-dimensional KV tiling (the Blackwell kernel), dynamic KV
+ * tiling or 1-D tiling of the row-major order -- and
+ * reports the speedup upper bound dense_tiles / max visited.
+ * Dilation is not simulated (the paper's simulator is described for window,
+ * stride and causal masks over Q/KV tile shapes).
+ * ------------------------------------------------------------------------ */
+#define GNA_SIM_STATIC 0
+#define GNA_SIM_DYNAMIC 1
+#define GNA_SIM_1D 2
+
+typedef struct gna_sim_args {
+    int spatial[3], window[3], stride[3], causal[3];
+    int q_tile[3], kv_tile[3]; /* T_Q, T_KV per axis (1-D mode: their products) */
+    int tiling;                /* GNA_SIM_STATIC / GNA_SIM_DYNAMIC / GNA_SIM_1D */
+    int n_extra;               /* extra (text) KV tokens, always visited */
+} gna_sim_args;
+
+typedef struct gna_sim_report {
+    long long dense_tiles;     /* KV tiles a dense kernel visits per Q tile */
+    long long visited_max;     /* worst Q tile */
+    double visited_mean;
+    long long n_q_tiles;
+    double bound;              /* (dense + extra) / (visited_max + extra): NATTENSim speedup */
+    double bound_mean;         /* mean-based (diagnostic, not the paper's bound) */
+    double flopwise;           /* 1 / (1 - sparsity) */
+    int perfectly_block_sparse;/* 1/0 for static tiling, -1 when not evaluated */
+    double kept_pairs;         /* attended (q, k) pairs */
+    double computed_pairs;     /* pairs inside visited tiles (incl. padding) */
+    double masked_fraction;    /* 1 - kept / computed */
+} gna_sim_report;
+
+/* Simulate one configuration.  GNA_EINVAL on invalid tiles/params (s <= w <= L). */
+int gna_sim(const gna_sim_args *a, gna_sim_report *r);
+/* Sweep every stride vector s_a in [1, w_a] and keep, grouped by stride product,
+ * only configurations whose bound strictly exceeds every smaller product's
+ * (P:779-790).  Writes up to `capacity` results (strides int32 [n][3]) and the
+ * number kept to *n_out (call with capacity 0 to size). */
+int gna_sim_sweep(const gna_sim_args *a, int32_t *strides_out, gna_sim_report *reports_out, int capacity,
+                  int *n_out);
+/* End-to-end Amdahl model of Tabs.2-4: self-attention share sa_share, sa_steps of
+ * `steps` diffusion steps kept dense, the rest sped up by op_speedup. */
+double gna_sim_e2e(double sa_share, int steps, int sa_steps, double op_speedup);
+
 /* Full forward: permute -> attention -> inverse permute, on the legacy default
  * stream with the library workspace.  Arguments as in gna_args. */
 int gna_forward(const void *q, const void *k, const void *v, void *out, float *lse,

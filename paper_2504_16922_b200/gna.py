@@ -55,6 +55,7 @@ EXPORTS = [
     "gna_forward", "gna_forward_ex", "gna_permute", "gna_attention_permuted", "gna_unpermute",
     "gna_workspace_size", "gna_plan_info", "gna_debug_windows", "gna_debug_visits", "gna_debug_worklist",
     "gna_release_workspace", "gna_last_error", "gna_device_supported", "gna_version",
+    "gna_sim", "gna_sim_sweep", "gna_sim_e2e",
 ]
 
 _lib = None

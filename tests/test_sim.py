@@ -1,0 +1,108 @@
+"""Product NATTENSim (csrc/sim.cpp) vs the oracle's simulator and the
+paper's printed tables (§3.2, Tab.3, Tab.4)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+
+
+@pytest.fixture(scope="module")
+def sim():
+    from paper_2504_16922_b200 import build
+
+    build.build()
+    from paper_2504_16922_b200 import sim as S
+
+    return S
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_static_matches_oracle_bruteforce_sim(sim, seed):
+    rng = np.random.default_rng(500 + seed)
+    L = [int(x) for x in rng.integers(2, 40, 3)]
+    w = [int(rng.integers(1, l + 1)) for l in L]
+    s = [int(rng.integers(1, x + 1)) for x in w]
+    causal = [bool(x) for x in rng.integers(0, 2, 3)]
+    tq = [int(rng.choice([1, 2, 4, 8])) for _ in L]
+    tk = [int(rng.choice([1, 2, 4, 8])) for _ in L]
+    r = sim.simulate(L, w, s, tq, tk, causal)
+    o = O.sim(O.Params(L, w, s, causal=causal), tq, tk)
+    assert r["dense_tiles"] == o["dense_tiles"]
+    assert r["visited_max"] == o["visited_max"]
+    assert r["visited_mean"] == pytest.approx(o["visited_mean"])
+    assert bool(r["perfectly_block_sparse"]) == o["perfectly_block_sparse"]
+    tot, _ = O.count_pairs(O.Params(L, w, s, causal=causal))
+    assert r["kept_pairs"] == tot
+
+
+def test_tab3_and_tab4_cells(sim):
+    g3, f = GOLD["tab3_hunyuan_91"], GOLD["fig4_hunyuan"]
+    for row in g3["rows"]:
+        r = sim.simulate(f["spatial"], f["window"], row["stride"], f["tq"], f["tk"])
+        assert abs(sim.e2e(g3["sa_share"], g3["steps"], row["sa_steps"], r["bound"]) - row["natten_sim"]) <= 0.008
+        assert abs(sim.e2e(g3["sa_share"], g3["steps"], row["sa_steps"], r["flopwise"]) - row["flopwise"]) <= 0.005
+    g4 = GOLD["tab4_flux_4k"]
+    for row in g4["rows"]:
+        r = sim.simulate(g4["spatial"], g4["window"], row["stride"], (16, 16), (16, 8))
+        assert abs(sim.e2e(g4["sa_share"], g4["steps"], row["sa_steps"], r["bound"]) - row["natten_sim"]) <= 0.005
+
+
+def test_design_dominance(sim):
+    """dynamic KV tiling <= static <= 1-D tiling (SPEC tiler-sim)."""
+    rng = np.random.default_rng(11)
+    for _ in range(15):
+        L = [int(x) for x in rng.integers(4, 24, 2)] + [1]
+        w = [int(rng.integers(1, l + 1)) for l in L[:2]] + [1]
+        s = [int(rng.integers(1, x + 1)) for x in w]
+        t = [int(rng.choice([2, 4])) for _ in range(2)] + [1]
+        st = sim.simulate(L, w, s, t, t)
+        dy = sim.simulate(L, w, s, t, t, tiling="dynamic")
+        assert dy["visited_max"] <= st["visited_max"]
+    # Fig.3 / P:308-347 ("curse of multi-dimensionality"): on the paper's video / image shapes
+    # 1-D tiling of the row-major order visits more KV tiles than multi-D tiles of the same
+    # volume.  (Not universal: on SPEC's tiny 8x8 example 1-D tiling visits 8 < 9.)
+    for L, w, t in (((48, 80), (24, 24), (8, 8)), ((64, 64), (32, 32), (8, 8)),
+                    ((30, 48, 80), (18, 24, 24), (2, 8, 8))):
+        one = sim.simulate(L, w, [1] * len(L), t, t, tiling="1d")["visited_max"]
+        multi = sim.simulate(L, w, [1] * len(L), t, t)["visited_max"]
+        assert one > multi
+
+
+def test_dynamic_perfect_block_sparsity_rule(sim):
+    """under dynamic KV tiling, T_KV | w and T_Q | s give the FLOP-wise speedup."""
+    r = sim.simulate((32, 48, 80), (16, 24, 24), (16, 8, 8), (4, 8, 8), (2, 8, 8), tiling="dynamic")
+    assert r["bound"] == pytest.approx(r["flopwise"])
+    r = sim.simulate((32, 48, 80), (16, 24, 24), (1, 1, 1), (4, 8, 8), (2, 8, 8), tiling="dynamic")
+    assert r["bound"] < r["flopwise"]
+
+
+def test_sweep_pruning(sim):
+    """the sweep keeps stride 1, bounds strictly increase with stride product,
+    and the Hunyuan shape contains a perfectly block-sparse point at x11.1 (Fig.4)."""
+    f = GOLD["fig4_hunyuan"]
+    res = sim.sweep(f["spatial"], f["window"], f["tq"], f["tk"])
+    assert res[0]["stride"] == [1, 1, 1]
+    b = [r["bound"] for r in res]
+    prods = [int(np.prod(r["stride"])) for r in res]
+    for i in range(1, len(res)):
+        if prods[i] > prods[i - 1]:
+            assert b[i] > max(b[:i]) - 1e-12
+    assert any(r["perfectly_block_sparse"] == 1 and round(r["bound"], 1) == 11.1 for r in res)
+    # SPEC example: 1-D L=8, w=8, T=4: s=8 (speedup 1, as s=1) is pruned
+    one = sim.sweep((8,), (8,), (4,), (4,))
+    assert [r["stride"][0] for r in one] == [1]
+
+
+def test_extra_tokens_dilute(sim):
+    """Extra (text) KV tiles are always visited: both speedups weakly decrease toward 1."""
+    base = sim.simulate((64, 64), (32, 32), (16, 16), (16, 8), (8, 8))
+    prev = base
+    for t in (64, 512, 4096):
+        r = sim.simulate((64, 64), (32, 32), (16, 16), (16, 8), (8, 8), n_extra=t)
+        assert 1.0 <= r["bound"] <= prev["bound"] and 1.0 <= r["flopwise"] <= prev["flopwise"]
+        prev = r
