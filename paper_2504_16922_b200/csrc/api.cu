@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -352,6 +353,29 @@ std::shared_ptr<Plan> get_plan(const gna_args* a) {
     return plan;
 }
 
+// Persistent-kernel work queue counters: a per-device ring, one counter per launch
+// (zeroed on the launch stream), so concurrent launches on different streams do
+// not share a counter unless more than kCounters are in flight.
+constexpr int kCounters = 4096;
+std::mutex g_ctr_mu;
+std::map<int, std::pair<int*, unsigned>> g_ctr;
+
+int next_counter(int** out) {
+    int dev = 0;
+    GNA_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_ctr_mu);
+    auto& e = g_ctr[dev];
+    if (!e.first) GNA_CUDA_TRY(cudaMalloc(&e.first, kCounters * sizeof(int)));
+    *out = e.first + (e.second++ % kCounters);
+    return GNA_OK;
+}
+
+bool use_persistent() {
+    // default on; GNA_PERSISTENT=0 selects the one-CTA-per-work-item kernel (A/B, debugging)
+    const char* v = getenv("GNA_PERSISTENT");
+    return !(v && v[0] == '0');
+}
+
 // per-device copy of the work list
 int plan_device_items(Plan& p, int4** out) {
     int dev = 0;
@@ -576,6 +600,8 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.direct = direct ? 1 : 0;
     p.n_extra = a->n_extra > 0 ? a->n_extra : 0;
     p.extra_stages = (p.n_extra + 127) / 128;
+    p.sched_counter = nullptr;
+    if (use_persistent() && (rc = next_counter(&p.sched_counter))) return rc;
     p.g = c.g;
     p.items = items;
     p.n_items = static_cast<long long>(c.plan->items.size());

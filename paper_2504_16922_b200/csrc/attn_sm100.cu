@@ -609,6 +609,8 @@ __global__ void __launch_bounds__(384, 1)
     }
 }
 
+#include "attn_persistent.cuh"
+
 template <int DP, int BV>
 static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
@@ -622,6 +624,28 @@ static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CU
         configured = true;
     }
     if (n_ctas <= 0) return cudaSuccess;
+    if (p.sched_counter != nullptr) {
+        static bool pconfigured = false;
+        if (!pconfigured) {
+            cudaError_t e = cudaFuncSetAttribute(gna_attn_sm100_persistent<DP, BV>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+            if (e != cudaSuccess) return e;
+            pconfigured = true;
+        }
+        static int sms = 0;
+        if (sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+        }
+        const long long grid = n_ctas < sms ? n_ctas : sms;
+        cudaError_t e = cudaMemsetAsync(p.sched_counter, 0, sizeof(int), stream);
+        if (e != cudaSuccess) return e;
+        gna_attn_sm100_persistent<DP, BV>
+            <<<static_cast<unsigned>(grid), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
+        return cudaGetLastError();
+    }
     gna_attn_sm100<DP, BV><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
     return cudaGetLastError();
 }

@@ -21,6 +21,7 @@ struct AttnParams {
     int direct;             // 1: Q/K/V tensor maps are 5-D maps over the user tensors (no permute pass)
     int n_extra;            // extra (text) KV tokens per (batch, head), appended as dense stages
     int extra_stages;       // ceil(n_extra / 128)
+    int* sched_counter;     // non-null: persistent kernel with a dynamic work queue (zeroed per launch)
     void* out_nat;          // if non-null: fused inverse permutation, O written to the user layout
     float* lse_nat;         //   and LSE likewise (may be null)
 };

@@ -25,10 +25,14 @@ def run(workloads, names):
     res = {}
     for rep in range(2):
         for name in names:
-            lib = os.path.join(VDIR, f"libgna_{name}.so") if name != "base" else os.path.join(
+            lname, _, envspec = name.partition("@")  # NAME@VAR=VAL[,VAR=VAL]: extra environment
+            lib = os.path.join(VDIR, f"libgna_{lname}.so") if lname != "base" else os.path.join(
                 ROOT, "paper_2504_16922_b200", "libgna_b200.so")
             for wl in workloads.split(","):
                 env = dict(os.environ, GNA_LIB_PATH=lib)
+                for kv in filter(None, envspec.split(",")):
+                    k, _, v = kv.partition("=")
+                    env[k] = v
                 out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", wl, "--steps", "10",
                                       "--warmup", "3", "--no-cpu-baseline"], env=env, capture_output=True, text=True,
                                      timeout=600)
