@@ -79,8 +79,10 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t bar_pc0 = bar_o_empty0 + 16;              // [2][3] P chunks (GNA_PSPLIT)
     const uint32_t bar_it_full0 = bar_pc0 + 48;              // [2] work queue
     const uint32_t bar_it_empty0 = bar_it_full0 + 16;        // [2]
-    long long* item_q = reinterpret_cast<long long*>(sgen + C::BAR_OFF + 16 + 16 * C::NS + 128);  // [2]
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 16 + 16 * C::NS + 144);
+    // barriers end at bar_it_empty0 + 16 = BAR_OFF + 160 + 16 * NS; then the queue entries
+    long long* item_q = reinterpret_cast<long long*>(sgen + C::BAR_OFF + 160 + 16 * C::NS);  // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 176 + 16 * C::NS);
+    static_assert(176 + 16 * C::NS + 4 <= 512, "barrier region overflow");
 
     if (threadIdx.x == 0) {
         GT(0, 15);
