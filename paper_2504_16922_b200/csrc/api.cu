@@ -371,9 +371,10 @@ int next_counter(int** out) {
 }
 
 bool use_persistent() {
-    // default on; GNA_PERSISTENT=0 selects the one-CTA-per-work-item kernel (A/B, debugging)
+    // default off (measured 12-25% slower on every config, profiles/r01_p1_ab_persistent.txt);
+    // GNA_PERSISTENT=1 selects the persistent work-queue kernel for A/B
     const char* v = getenv("GNA_PERSISTENT");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
 }
 
 // per-device copy of the work list
