@@ -370,6 +370,15 @@ int next_counter(int** out) {
     return GNA_OK;
 }
 
+// Attention kernel selection: "v4" (default, attn_v4.cu), "v3" (one CTA per work item,
+// attn_sm100.cu), "v3p" (v3 with the persistent work queue).  GNA_KERNEL overrides.
+int kernel_choice() {
+    const char* v = getenv("GNA_KERNEL");
+    if (v && strcmp(v, "v3") == 0) return 3;
+    if (v && strcmp(v, "v3p") == 0) return 2;
+    return 4;
+}
+
 bool use_persistent() {
     // default off (measured 12-25% slower on every config, profiles/r01_p1_ab_persistent.txt);
     // GNA_PERSISTENT=1 selects the persistent work-queue kernel for A/B
@@ -602,7 +611,8 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.n_extra = a->n_extra > 0 ? a->n_extra : 0;
     p.extra_stages = (p.n_extra + 127) / 128;
     p.sched_counter = nullptr;
-    if (use_persistent() && (rc = next_counter(&p.sched_counter))) return rc;
+    const int kc = kernel_choice();
+    if ((kc == 2 || (kc == 3 && use_persistent())) && (rc = next_counter(&p.sched_counter))) return rc;
     p.g = c.g;
     p.items = items;
     p.n_items = static_cast<long long>(c.plan->items.size());
@@ -619,7 +629,8 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out_nat = fused_out ? a->out : nullptr;
     p.lse_nat = fused_out ? a->lse : nullptr;
-    GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, tek, tev, we - wb, c.st));
+    if (kc == 4) GNA_CUDA_TRY(launch_attention_v4(p, tq, tk, tv, tek, tev, c.st));
+    else GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, tek, tev, we - wb, c.st));
     return post_launch(a, c.st, "gna_attn_sm100");
 }
 

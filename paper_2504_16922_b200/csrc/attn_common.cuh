@@ -1,0 +1,145 @@
+// attn_common.cuh -- helpers shared by the attention kernels (attn_sm100.cu,
+// attn_v4.cu): trace macros, compile-time variant knobs, stage decoding and
+// the separable GNA row mask over a box (P:627-628 fine-grained masking).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "geom.cuh"
+#include "kernels.h"
+#include "ptx.cuh"
+
+// Optional cycle tracing of the pipeline (build with -DGNA_TRACE, see
+// scripts/trace_attn.py): per CTA < 4, per stage, clock64() at pipeline events.
+#ifdef GNA_TRACE
+#define GNA_TRACE_CTAS 4
+#define GNA_TRACE_STAGES 256
+static __device__ unsigned long long g_gna_trace[GNA_TRACE_CTAS][GNA_TRACE_STAGES][16];
+#define GT(j, ev)                                                                      \
+    do {                                                                               \
+        if (blockIdx.x < GNA_TRACE_CTAS && (j) < GNA_TRACE_STAGES)                     \
+            g_gna_trace[blockIdx.x][(j)][(ev)] = clock64();                           \
+    } while (0)
+// per-CTA timeline (all CTAs < GNA_TL_CTAS): globaltimer ns at events, plus the SM id
+#define GNA_TL_CTAS 8192
+static __device__ unsigned long long g_gna_tl[GNA_TL_CTAS][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define GTL(ev)                                                                        \
+    do {                                                                               \
+        if (blockIdx.x < GNA_TL_CTAS) g_gna_tl[blockIdx.x][(ev)] = gtimer();           \
+    } while (0)
+#define GTLW(w, ev)                                                                    \
+    do {                                                                               \
+        if ((w) < GNA_TL_CTAS) g_gna_tl[(w)][(ev)] = gtimer();                         \
+    } while (0)
+#else
+#define GTL(ev) \
+    do {        \
+    } while (0)
+#define GTLW(w, ev) \
+    do {            \
+    } while (0)
+#define GT(j, ev) \
+    do {          \
+    } while (0)
+#endif
+
+// Compile-time variants for A/B measurements (scripts/ab.py); defaults are the
+// measured best.
+#ifndef GNA_POLY_EVERY
+#define GNA_POLY_EVERY 8  // 1 exp pair in GNA_POLY_EVERY on the FMA pipe (0 = all MUFU)
+#endif
+#ifndef GNA_NS128
+#define GNA_NS128 4  // K/V ring slots of 32 KB at head_dim 128
+#endif
+#ifndef GNA_PSPLIT
+#define GNA_PSPLIT 2  // P is handed to the MMA in GNA_PSPLIT chunks (1, 2 or 4): the PV of the
+                      // first keys starts while the softmax still computes the last ones
+#endif
+
+namespace gna {
+namespace attn {
+
+template <int DP, int BV>
+struct Cfg {
+    static constexpr int NH = DP / 64;               // 128-byte column chunks ("halves")
+    static constexpr int CHUNK_BYTES = 128 * 128;    // 128 rows x 128 B, one SW128 chunk
+    static constexpr int TILE_BYTES = NH * CHUNK_BYTES;  // 128 rows x DP bf16
+    static constexpr int NS = DP == 128 ? GNA_NS128 : 8;  // KV ring slots (K and V share it)
+    static constexpr int KPB = 128 / BV;             // boxes per 128-row tile
+    static constexpr int Q_OFF = 0;
+    static constexpr int KV_OFF = 2 * TILE_BYTES;
+    static constexpr int BAR_OFF = KV_OFF + NS * TILE_BYTES;
+    static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
+    static constexpr int THREADS = 384;
+};
+
+struct StageBoxes {
+    int k[2][3];   // box coordinates (class-local box units) of the stage's boxes
+    int dead[2];   // 1 = filler box (odd count), masked entirely
+    int lin[2];    // linear box index inside the class box grid
+};
+
+__device__ __forceinline__ void decode_stage(const Geometry& g, const int lo[3], const int ext[3], int nkv,
+                                             int j, int kpb, StageBoxes& sb) {
+    for (int u = 0; u < kpb; ++u) {
+        int jb = j * kpb + u;
+        sb.dead[u] = jb >= nkv;
+        if (jb >= nkv) jb = 0;
+        const int k2 = jb % ext[2];
+        const int k1 = (jb / ext[2]) % ext[1];
+        const int k0 = jb / (ext[2] * ext[1]);
+        sb.k[u][0] = lo[0] + k0;
+        sb.k[u][1] = lo[1] + k1;
+        sb.k[u][2] = lo[2] + k2;
+        sb.lin[u] = ((lo[0] + k0) * g.nb[1] + (lo[1] + k1)) * g.nb[2] + (lo[2] + k2);
+    }
+}
+
+// ---- separable GNA mask of one row over one box, as a bit mask over the
+// box's rows (row-major (i0, i1, i2)).  Axis intervals [lo, hi) are relative
+// to the box origin.  Built from per-axis interval masks by multiplying with
+// "comb" constants (no carries: the operands occupy disjoint bit fields).
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ u128 bits_below(int n) {  // n in [0, 128]
+    return n >= 128 ? ~static_cast<u128>(0) : ((static_cast<u128>(1) << n) - 1);
+}
+__device__ __forceinline__ u128 bit_range(int a, int b) { return bits_below(b) & ~bits_below(a); }
+
+struct BoxMaskConsts {
+    u128 comb1;  // bit i1*B2 for i1 < B1
+    u128 comb0;  // bit i0*B1*B2 for i0 < B0
+};
+
+__device__ __forceinline__ BoxMaskConsts box_mask_consts(const Geometry& g) {
+    BoxMaskConsts c;
+    c.comb1 = 0;
+    c.comb0 = 0;
+    for (int i = 0; i < g.B[1]; ++i) c.comb1 |= static_cast<u128>(1) << (i * g.B[2]);
+    for (int i = 0; i < g.B[0]; ++i) c.comb0 |= static_cast<u128>(1) << (i * g.B[1] * g.B[2]);
+    return c;
+}
+
+__device__ __forceinline__ u128 box_row_mask(const Geometry& g, const BoxMaskConsts& mc, const int lo[3],
+                                             const int hi[3]) {
+    int a[3], b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a[k] = max(lo[k], 0);
+        b[k] = min(hi[k], g.B[k]);
+        if (a[k] >= b[k]) return 0;
+    }
+    const u128 m2 = bit_range(a[2], b[2]);
+    const u128 m12 = (m2 * mc.comb1) & bit_range(a[1] * g.B[2], b[1] * g.B[2]);
+    const int s01 = g.B[1] * g.B[2];
+    return (m12 * mc.comb0) & bit_range(a[0] * s01, b[0] * s01);
+}
+
+}  // namespace attn
+}  // namespace gna

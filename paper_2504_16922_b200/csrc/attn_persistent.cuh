@@ -147,6 +147,14 @@ __global__ void __launch_bounds__(384, 1)
                 *reinterpret_cast<volatile long long*>(&item_q[slot]) = w;
                 ptx::mbar_arrive(bar_it_full0 + 8 * slot);
                 if (w < 0) break;
+                GTLW(w, 0);
+#ifdef GNA_TRACE
+                if (w < GNA_TL_CTAS) {
+                    unsigned smid;
+                    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+                    g_gna_tl[w][7] = smid;
+                }
+#endif
                 decode_item<KPB>(p, w, wi);
                 if (wi.nst <= 0) continue;
                 const bool hasB = wi.subB >= 0;
@@ -171,6 +179,7 @@ __global__ void __launch_bounds__(384, 1)
                 };
                 // Q buffers free once every QK^T of the previous item has completed
                 if (n_local > 0) ptx::mbar_wait(bar_q_empty, (n_local - 1) & 1);
+                GTLW(w, 1);
                 ptx::mbar_expect_tx(bar_q_full, (hasB ? 2 : 1) * C::TILE_BYTES);
                 for (int i = 0; i < (hasB ? 2 : 1); ++i) {
                     int sc[3];
@@ -291,6 +300,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             ptx::mma_commit(bar_o_full0);
+            GTLW(w, 5);
             ++n_o[0];
             if (hasB) {
                 ptx::mma_commit(bar_o_full0 + 8);
@@ -369,6 +379,7 @@ __global__ void __launch_bounds__(384, 1)
 
             ptx::mbar_wait(bar_s, cnt & 1);
             if (r == 0 && first) GT(j, 4 * i + 0);
+            if (r == 0 && i == 0 && j == 0) GTLW(w, 2);
             ptx::tc_fence_after();
             float s[128];
 #pragma unroll
@@ -461,6 +472,7 @@ __global__ void __launch_bounds__(384, 1)
             ++cnt;
         }
         first = false;
+        if (r == 0 && i == 0) GTLW(w, 3);
 
         // ---------------------------------------------------------- epilogue
         ptx::mbar_wait(bar_o_full0 + 8 * i, n_done & 1);
@@ -508,6 +520,7 @@ __global__ void __launch_bounds__(384, 1)
                 *lrow = (m_eff + __log2f(l_run)) * 0.69314718055994530942f;
             }
         }
+        if (r == 0 && i == 0) GTLW(w, 4);
       }
     }
 

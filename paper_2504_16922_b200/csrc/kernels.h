@@ -35,6 +35,11 @@ cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const C
                              const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
                              cudaStream_t stream);
 
+// persistent kernel (attn_v4.cu): one CTA per SM, tasks = 128-row Q sub-tiles of the work range
+cudaError_t launch_attention_v4(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
+                                const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev,
+                                cudaStream_t stream);
+
 // q/k/v natural [B][s0][s1][s2][H][D] -> permuted [BH][C][nbox][box_vol][Dp]
 cudaError_t launch_permute_qkv(const Geometry& g, const void* q, const void* k, const void* v, void* qp,
                                void* kp, void* vp, cudaStream_t stream);

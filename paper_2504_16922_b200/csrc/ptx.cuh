@@ -3,6 +3,9 @@
 // Raw PTX, no CUTLASS/CuTe.  Compile with -gencode arch=compute_100a,code=sm_100a.
 #pragma once
 #include <stdint.h>
+#ifdef GNA_HANG_DEBUG
+#include <cstdio>
+#endif
 
 namespace gna {
 namespace ptx {
@@ -25,6 +28,37 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+#ifdef GNA_HANG_DEBUG
+// debug build: per-CTA progress words written by the kernels (GNA_PROG), printed on a hang
+__device__ int g_prog[2048][8];
+#define GNA_PROG(slot, val)                                                              \
+    do {                                                                                 \
+        if (blockIdx.x < 2048) *(volatile int*)&::gna::ptx::g_prog[blockIdx.x][(slot)] = (val); \
+    } while (0)
+// debug build: bounded spin, then report the stuck barrier (smem offset) and trap
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    for (long long n = 0;; ++n) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (n == (1ll << 22) && (threadIdx.x & 31) == 0)
+            printf("HANG block %d thread %d bar smem 0x%x parity %u prog %d %d %d %d %d %d %d %d\n", blockIdx.x,
+                   threadIdx.x, bar, parity, g_prog[blockIdx.x][0], g_prog[blockIdx.x][1], g_prog[blockIdx.x][2],
+                   g_prog[blockIdx.x][3], g_prog[blockIdx.x][4], g_prog[blockIdx.x][5], g_prog[blockIdx.x][6],
+                   g_prog[blockIdx.x][7]);
+        if (n == (1ll << 25)) asm volatile("trap;");
+    }
+}
+#else
+#define GNA_PROG(slot, val) \
+    do {                    \
+    } while (0)
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -34,6 +68,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#endif
 
 // ---------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* desc) {

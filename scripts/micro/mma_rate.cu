@@ -64,7 +64,23 @@ __global__ void kern(int iters, long long* cyc, const uint8_t* gsrc) {
         const uint32_t idesc = ptx::idesc_bf16(128, N, 0, 0);
         const uint32_t a = base, b = base + 32768;
         long long t0 = clock64();
-        for (int it = 0; it < iters; ++it) {
+        if (MODE == 2) {
+            // planned 64-key stage: S = Q K^T (SS, N=64, K=128: 8 instrs) then O += P V (TS, N=128, K=64: 4 instrs)
+            const uint32_t idesc64 = ptx::idesc_bf16(128, 64, 0, 0);
+            const uint32_t idesc128v = ptx::idesc_bf16(128, 128, 0, 1);
+            for (int it = 0; it < iters; ++it) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32 + ((it & 1) ? 32768 : 0);
+                    ptx::mma_ss(tmem + 128, ptx::smem_desc_sw128(a + off, 16, 1024),
+                                ptx::smem_desc_sw128(b + off, 16, 1024), idesc64, 1);
+                }
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    ptx::mma_ts(tmem, tmem + 192 + kk * 8, ptx::smem_desc_sw128(b + kk * 2048, 16384, 1024), idesc128v, 1);
+            }
+        }
+        for (int it = 0; it < (MODE == 2 ? 0 : iters); ++it) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
                 const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32 + ((it & 1) ? 32768 : 0);
@@ -95,6 +111,10 @@ void run(const char* name) {
     long long h[148]; cudaMemcpy(h, cyc, 148 * 8, cudaMemcpyDeviceToHost);
     double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
     const double per = avg / (iters * 8.0);
+    if (MODE == 2)
+        printf("%s warps=%d tma=%d MIXED 8xSS(N64)+4xTS(N128): %.1f cycles per stage (ideal 512) -> %.0f FLOP/clk/SM\n",
+               STORE ? "STTM" : "LDTM", LOADERS, TMA, avg / iters, 2.0 * 128 * 64 * 128 * 2 / (avg / iters));
+    else
     printf("%s warps=%d tma=%d %-4s N=%3d: %.1f cycles per M128xNxK16 MMA -> %.0f FLOP/clk/SM\n", STORE ? "STTM" : "LDTM", LOADERS, TMA, name, N, per, 2.0 * 128 * N * 16 / per);
     cudaFree(cyc);
 }
@@ -102,6 +122,9 @@ void run(const char* name) {
 int main() {
     cudaMalloc(&g_src, 32ll << 20);
     cudaMemset(g_src, 0, 32ll << 20);
+    run<0, 64>("SS"); run<1, 64>("TS"); run<0, 256>("SS"); run<1, 256>("TS");
+    run<2, 64>("MIX"); run<2, 64, 8>("MIX"); run<2, 64, 8, 1>("MIX"); run<2, 64, 8, 0, 1>("MIX");
+    run<0, 64, 8>("SS"); run<0, 64, 0, 0, 1>("SS"); run<0, 64, 8, 0, 1>("SS");
     run<0, 128>("SS"); run<1, 128>("TS");
     run<0, 128, 8>("SS"); run<1, 128, 8>("TS");
     run<0, 128, 8, 1>("SS"); run<1, 128, 8, 1>("TS");
