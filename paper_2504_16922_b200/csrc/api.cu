@@ -370,13 +370,16 @@ int next_counter(int** out) {
     return GNA_OK;
 }
 
-// Attention kernel selection: "v4" (default, attn_v4.cu), "v3" (one CTA per work item,
-// attn_sm100.cu), "v3p" (v3 with the persistent work queue).  GNA_KERNEL overrides.
+// Attention kernel selection (GNA_KERNEL): "v3" (default: one CTA per work item of two
+// 128-row sub-tiles, attn_sm100.cu), "v3p" (v3 with the persistent work queue), "v4"
+// (experimental persistent single-sub-tile kernel, attn_v4.cu).  Measured on B200
+// (profiles/r01_v4_ab.txt): v4 moves 4x the L2 bytes of v3 (K/V reused by 128 rows instead
+// of 256) and its two key-half softmax warps per SMSP run in lockstep, so it is 1.4-2x slower.
 int kernel_choice() {
     const char* v = getenv("GNA_KERNEL");
-    if (v && strcmp(v, "v3") == 0) return 3;
+    if (v && strcmp(v, "v4") == 0) return 4;
     if (v && strcmp(v, "v3p") == 0) return 2;
-    return 4;
+    return 3;
 }
 
 bool use_persistent() {
@@ -624,6 +627,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.work_begin = wb;
     p.work_end = we;
     p.o_perm = c.ws ? c.ws + c.L.o : nullptr;
+    p.q_src = direct ? a->q : (c.ws ? c.ws + c.L.q : nullptr);
     p.lse_perm = c.ws ? reinterpret_cast<float*>(c.ws + c.L.lse) : nullptr;
     const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));
     p.scale_log2 = scale * 1.4426950408889634f;

@@ -25,12 +25,12 @@
 //     small problems.
 //
 // Warp roles (512 threads, registers re-balanced with setmaxnreg):
-//   warps 0-3   softmax, key half 0 (keys 0..63 of each 128-key stage)   160 regs
+//   warps 0-3   softmax, key half 0 (keys 0..63 of each 128-key stage)   168 regs
 //   warps 4-7   softmax, key half 1 (keys 64..127); warps w and w+4 own the same rows
 //   warp  8     TMA producer: K_j, V_j into a smem ring                   72 regs
 //   warp  9     MMA issuer (one lane): S = Q K^T (TS), O += P V (TS)
-//   warp  10    TMA producer: Q sub-tile into the smem staging buffer
-//   warps 12-15 Q stager (smem -> TMEM) and epilogue (O, LSE -> HBM)      120 regs
+//   warps 12-15 Q stager (HBM -> registers -> TMEM, one task ahead) and
+//               epilogue (O, LSE -> HBM)                                  104 regs
 // TMEM (512 columns x 128 lanes): Q0 [0,64) Q1 [64,128) S0 [128,256)
 //   S1 [256,384) O [384,512).  P(j) (bf16x2) overwrites the first 32 columns
 //   of each key half of its S buffer: half h at S_b + 64h.
@@ -50,10 +50,23 @@ static __device__ unsigned long long g_v4_tl[GNA_TL_CTAS][8];
     do {                                                               \
         if ((tau) < GNA_TL_CTAS) g_v4_tl[(tau)][(ev)] = gtimer();      \
     } while (0)
+// per-stage pipeline events of CTAs < 4 (clock64), same buffer layout as the v3 trace
+static __device__ unsigned long long g_v4_tr[4][256][16];
+#define GT4(t, ev)                                                                 \
+    do {                                                                           \
+        if (blockIdx.x < 4 && (t) < 256) g_v4_tr[blockIdx.x][(t)][(ev)] = clock64(); \
+    } while (0)
 #else
+#define GT4(t, ev) \
+    do {           \
+    } while (0)
 #define TL4(tau, ev) \
     do {             \
     } while (0)
+#endif
+
+#ifndef GNA_V4_PF
+#define GNA_V4_PF 4
 #endif
 
 template <int DP>
@@ -61,10 +74,10 @@ struct Cfg4 {
     static constexpr int NH = DP / 64;                   // 128-byte column chunks
     static constexpr int CHUNK = 128 * 128;              // 128 rows x 128 B (one SW128 chunk)
     static constexpr int TILE = NH * CHUNK;              // 128 rows x DP bf16
-    static constexpr int NS = DP == 128 ? 5 : 8;         // K/V ring slots
+    static constexpr int NS = DP == 128 ? 6 : 10;        // K/V ring slots (192 / 160 KB)
+    static constexpr int PF = GNA_V4_PF;                 // K/V stages prefetched into L2 ahead of the ring
     static constexpr int QCOLS = DP / 2;                 // TMEM columns of one Q buffer
-    static constexpr int Q_OFF = 0;                      // Q staging
-    static constexpr int KV_OFF = TILE;
+    static constexpr int KV_OFF = 0;
     static constexpr int BAR_OFF = KV_OFF + NS * TILE;
     static constexpr int NBAR = 17 + 2 * NS;
     static constexpr int HOLDER_OFF = BAR_OFF + 384;
@@ -186,11 +199,9 @@ __global__ void __launch_bounds__(512, 1)
     const int lane = threadIdx.x & 31;
     const long long ntask = 2 * (p.work_end - p.work_begin);
 
-    const uint32_t sQ = sbase + C::Q_OFF;
     const uint32_t sKV = sbase + C::KV_OFF;
     const uint32_t bar0 = sbase + C::BAR_OFF;
-    const uint32_t bar_q_full = bar0, bar_q_empty = bar0 + 8;
-    const uint32_t bar_qt_full0 = bar0 + 16;  // [2]
+    const uint32_t bar_qt_full0 = bar0 + 16;  // [2] Q of task parity staged in TMEM
     auto bar_kv_full = [&](int s) { return bar0 + 32u + 8u * s; };
     auto bar_kv_empty = [&](int s) { return bar0 + 32u + 8u * (C::NS + s); };
     const uint32_t bar_s_full0 = bar0 + 32u + 16u * C::NS;  // [2]
@@ -208,8 +219,6 @@ __global__ void __launch_bounds__(512, 1)
     float* xm = reinterpret_cast<float*>(sgen + C::XM_OFF);
 
     if (threadIdx.x == 0) {
-        ptx::mbar_init(bar_q_full, 1);
-        ptx::mbar_init(bar_q_empty, 128);
         ptx::mbar_init(bar_qt_full0, 128);
         ptx::mbar_init(bar_qt_full0 + 8, 128);
         for (int s = 0; s < C::NS; ++s) {
@@ -250,33 +259,70 @@ __global__ void __launch_bounds__(512, 1)
             const int c3 = ccls[1] + g.ax[1].d * k1 * g.B[1];
             const int c4 = static_cast<int>(b_idx * g.ax[0].L) + ccls[0] + g.ax[0].d * k0 * g.B[0];
 #pragma unroll
-            for (int h = 0; h < C::NH; ++h) ptx::tma_load_5d(dst + h * C::CHUNK, tm, bar, h * 64, h_idx, c2, c3, c4);
+            for (int h = 0; h < C::NH; ++h) ptx::tma_load_5d_e(dst + h * C::CHUNK, tm, bar, h * 64, h_idx, c2, c3, c4);
         } else {
             const int row = static_cast<int>(t.cls_row0 + static_cast<long long>((k0 * g.nb[1] + k1) * g.nb[2] + k2) * BV);
 #pragma unroll
-            for (int h = 0; h < C::NH; ++h) ptx::tma_load_2d(dst + h * C::CHUNK, tm, bar, h * 64, row);
+            for (int h = 0; h < C::NH; ++h) ptx::tma_load_2d_e(dst + h * C::CHUNK, tm, bar, h * 64, row);
         }
     };
 
     if (warp >= 8 && warp < 12) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 72;\n" ::: "memory");
-        if (warp == 8 && lane == 0) {
-            // ================================================= K/V producer
-            ptx::tma_prefetch_desc(&tmap_k);
-            ptx::tma_prefetch_desc(&tmap_v);
-            if (p.n_extra > 0) {
+        if (warp == 8) {
+            // ================================================= K/V producer (warp-uniform, one elected lane issues)
+            if (lane == 0) {
+                ptx::tma_prefetch_desc(&tmap_k);
+                ptx::tma_prefetch_desc(&tmap_v);
+            }
+            if (p.n_extra > 0 && lane == 0) {
                 ptx::tma_prefetch_desc(&tmap_ek);
                 ptx::tma_prefetch_desc(&tmap_ev);
             }
             long long it = 0;
             Task t;
+            // L2 prefetch of the K and V boxes of stage j + PF while stage j is loaded into the ring:
+            // the ring covers ~2 stages, the HBM latency under load is longer than that
+            auto prefetch_stage = [&](Odo& o) {
+#pragma unroll
+                for (int u = 0; u < KPB; ++u) {
+                    int c[3];
+                    bool dead;
+                    o.take(t, c, dead);
+                    if (dead) continue;
+                    if (p.direct) {
+                        int ccls[3];
+                        class_coords(g, t.cls, ccls);
+                        const int h_idx = static_cast<int>(t.bh % g.heads);
+                        const int c2 = ccls[2] + g.ax[2].d * c[2] * g.B[2];
+                        const int c3 = ccls[1] + g.ax[1].d * c[1] * g.B[1];
+                        const int c4 = static_cast<int>((t.bh / g.heads) * g.ax[0].L) + ccls[0] + g.ax[0].d * c[0] * g.B[0];
+#pragma unroll
+                        for (int hh = 0; hh < C::NH; ++hh) {
+                            ptx::tma_prefetch_5d_e(&tmap_k, hh * 64, h_idx, c2, c3, c4);
+                            ptx::tma_prefetch_5d_e(&tmap_v, hh * 64, h_idx, c2, c3, c4);
+                        }
+                    } else {
+                        const int row = static_cast<int>(
+                            t.cls_row0 + static_cast<long long>((c[0] * g.nb[1] + c[1]) * g.nb[2] + c[2]) * BV);
+#pragma unroll
+                        for (int hh = 0; hh < C::NH; ++hh) {
+                            ptx::tma_prefetch_2d_e(&tmap_k, hh * 64, row);
+                            ptx::tma_prefetch_2d_e(&tmap_v, hh * 64, row);
+                        }
+                    }
+                }
+            };
             for (long long tau = next_task<BV>(p, blockIdx.x, ntask, t); tau >= 0;
                  tau = next_task<BV>(p, tau + gridDim.x, ntask, t)) {
-                Odo od;
+                Odo od, opf;
                 od.reset(t.nkv);
+                opf.reset(t.nkv);
+                for (int j = 0; j < C::PF && j < t.nst_gna; ++j) prefetch_stage(opf);
                 const long long b_idx = t.bh / g.heads;
                 const int h_idx = static_cast<int>(t.bh % g.heads);
                 for (int j = 0; j < t.nst; ++j) {
+                    if (j + C::PF < t.nst_gna) prefetch_stage(opf);
                     int kc[KPB][3];
                     if (j < t.nst_gna) {
 #pragma unroll
@@ -288,7 +334,8 @@ __global__ void __launch_bounds__(512, 1)
                     for (int kind = 0; kind < 2; ++kind, ++it) {
                         const int slot = static_cast<int>(it % C::NS);
                         ptx::mbar_wait(bar_kv_empty(slot), static_cast<uint32_t>(((it / C::NS) & 1) ^ 1));
-                        ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE);
+                        if (lane == 0 && kind == 0) GT4(it / 2, 15);
+                        ptx::mbar_expect_tx_e(bar_kv_full(slot), C::TILE);
                         const uint32_t dst = sKV + slot * C::TILE;
                         if (j < t.nst_gna) {
                             const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
@@ -302,32 +349,13 @@ __global__ void __launch_bounds__(512, 1)
                             const int row = static_cast<int>(b_idx * p.n_extra) + (j - t.nst_gna) * 128;
 #pragma unroll
                             for (int h = 0; h < C::NH; ++h)
-                                ptx::tma_load_3d(dst + h * C::CHUNK, tm, bar_kv_full(slot), h * 64, h_idx, row);
+                                ptx::tma_load_3d_e(dst + h * C::CHUNK, tm, bar_kv_full(slot), h * 64, h_idx, row);
                         }
                     }
                 }
             }
-        } else if (warp == 10 && lane == 0) {
-            // ================================================= Q producer
-            ptx::tma_prefetch_desc(&tmap_q);
-            long long n = 0;
-            Task t;
-            for (long long tau = next_task<BV>(p, blockIdx.x, ntask, t); tau >= 0;
-                 tau = next_task<BV>(p, tau + gridDim.x, ntask, t), ++n) {
-                if (n > 0) ptx::mbar_wait(bar_q_empty, static_cast<uint32_t>((n - 1) & 1));
-                GNA_PROG(7, static_cast<int>(n));
-                ptx::mbar_expect_tx(bar_q_full, C::TILE);
-                int sc[3];
-                sub_coords(g, t.sub, sc);
-#pragma unroll
-                for (int u = 0; u < KPB; ++u) {
-                    const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
-                    load_box(&tmap_q, sQ + u * BV * 128, bar_q_full, t, sc[0] * g.QB[0] + u0, sc[1] * g.QB[1] + u1,
-                             sc[2] * g.QB[2] + u2);
-                }
-            }
-        } else if (warp == 9 && lane == 0) {
-            // ================================================= MMA issuer
+        } else if (warp == 9) {
+            // ================================================= MMA issuer (warp-uniform, one elected lane issues)
             constexpr uint32_t IDESC_QK = ptx::idesc_bf16(128, 128, 0, 0);
             constexpr uint32_t IDESC_PV = ptx::idesc_bf16(128, DP, 0, 1);
             struct Cur {
@@ -352,12 +380,14 @@ __global__ void __launch_bounds__(512, 1)
                 }
             };
             auto issue_s = [&](const Cur& c) {
-                GNA_PROG(5, static_cast<int>(c.t) * 16 + 1);
+                if (lane == 0) GNA_PROG(5, static_cast<int>(c.t) * 16 + 1);
+                if (lane == 0) GT4(c.t, 6);
                 const int qb = static_cast<int>(c.n & 1);
                 if (c.j == 0) ptx::mbar_wait(bar_qt_full0 + 8 * qb, static_cast<uint32_t>((c.n >> 1) & 1));
                 const long long it = 2 * c.t;
                 const int slot = static_cast<int>(it % C::NS);
                 ptx::mbar_wait(bar_kv_full(slot), static_cast<uint32_t>((it / C::NS) & 1));
+                if (lane == 0) GT4(c.t, 12);
                 ptx::tc_fence_after();
                 const uint32_t kb = sKV + slot * C::TILE;
                 const uint32_t dS = tmem + TM_S + 128 * static_cast<uint32_t>(c.t & 1);
@@ -365,14 +395,16 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                 for (int kk = 0; kk < DP / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * C::CHUNK + (kk & 3) * 32;
-                    ptx::mma_ts(dS, aQ + 8 * kk, ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
+                    ptx::mma_ts_elect(dS, aQ + 8 * kk, ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
                 }
-                ptx::mma_commit(bar_s_full0 + 8 * static_cast<uint32_t>(c.t & 1));
-                ptx::mma_commit(bar_kv_empty(slot));
-                GNA_PROG(5, static_cast<int>(c.t) * 16 + 2);
+                if (lane == 0) GT4(c.t, 8);
+                ptx::mma_commit_elect(bar_s_full0 + 8 * static_cast<uint32_t>(c.t & 1));
+                ptx::mma_commit_elect(bar_kv_empty(slot));
+                if (lane == 0) GNA_PROG(5, static_cast<int>(c.t) * 16 + 2);
             };
             auto issue_pv = [&](const Cur& c) {
-                GNA_PROG(6, static_cast<int>(c.t) * 16 + 1);
+                if (lane == 0) GNA_PROG(6, static_cast<int>(c.t) * 16 + 1);
+                if (lane == 0) GT4(c.t, 13);
                 if (c.j == 0 && c.n > 0) ptx::mbar_wait(bar_o_empty, static_cast<uint32_t>((c.n - 1) & 1));
                 const long long it = 2 * c.t + 1;
                 const int slot = static_cast<int>(it % C::NS);
@@ -382,19 +414,21 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     ptx::mbar_wait(bar_p_full0 + 8 * (2 * (c.t & 1) + h), static_cast<uint32_t>((c.t >> 1) & 1));
+                    if (lane == 0) GT4(c.t, 9 + h);
                     ptx::tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const int q = 4 * h + kk;  // 16-key chunk of the stage
-                        ptx::mma_ts(tmem + TM_O, aP + 64 * h + 8 * kk,
+                        ptx::mma_ts_elect(tmem + TM_O, aP + 64 * h + 8 * kk,
                                     ptx::smem_desc_sw128(vb + q * 2048, C::CHUNK, 1024), IDESC_PV,
                                     (c.j > 0 || q > 0) ? 1u : 0u);
                     }
                 }
-                ptx::mma_commit(bar_kv_empty(slot));
-                ptx::mma_commit(bar_pv_done);
-                if (c.j == c.nst - 1) ptx::mma_commit(bar_o_full);
-                GNA_PROG(6, static_cast<int>(c.t) * 16 + 2);
+                ptx::mma_commit_elect(bar_kv_empty(slot));
+                ptx::mma_commit_elect(bar_pv_done);
+                if (c.j == c.nst - 1) ptx::mma_commit_elect(bar_o_full);
+                if (lane == 0) GT4(c.t, 14);
+                if (lane == 0) GNA_PROG(6, static_cast<int>(c.t) * 16 + 2);
             };
             if (cs.tau >= 0) {
                 issue_s(cs);
@@ -414,36 +448,56 @@ __global__ void __launch_bounds__(512, 1)
             }
         }
     } else if (warp >= 12) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 120;\n" ::: "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
         // ===================================================== Q stager + epilogue
         const int r = threadIdx.x - 384;  // row == TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        auto stage_q = [&](long long n) {
+        // Q rows of task tq -> registers -> TMEM buffer n&1 (the A operand of QK^T: column c holds
+        // head-dim elements 2c, 2c+1 of the row, low half first -- the layout P uses for PV)
+        auto stage_q = [&](const Task& tq, long long n) {
             if (r == 0) GNA_PROG(4, static_cast<int>(n) * 16 + 1);
-            ptx::mbar_wait(bar_q_full, static_cast<uint32_t>(n & 1));
+            int cc[3], x[3], bxo[3], inner;
+            bool valid;
+            row_coords(g, tq.cls, tq.sub, r, BV, cc, x, valid, bxo, inner);
+            const uint4* src;
+            if (p.direct) {
+                long long tok = 0;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) tok = tok * g.ax[a].L + (cc[a] + static_cast<long long>(g.ax[a].d) * x[a]);
+                const long long N = static_cast<long long>(g.ax[0].L) * g.ax[1].L * g.ax[2].L;
+                const long long nat = ((tq.bh / g.heads) * N + tok) * g.heads + tq.bh % g.heads;
+                src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.q_src) + nat * g.D);
+            } else {
+                const long long row_g =
+                    tq.cls_row0 + static_cast<long long>((bxo[0] * g.nb[1] + bxo[1]) * g.nb[2] + bxo[2]) * BV + inner;
+                src = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.q_src) + row_g * DP);
+                valid = true;  // padding rows of the permuted buffer hold zeros
+            }
+            uint32_t wv[C::QCOLS];
+#pragma unroll
+            for (int u = 0; u < C::QCOLS / 4; ++u) {
+                const uint4 v4 = valid ? __ldg(src + u) : make_uint4(0, 0, 0, 0);
+                wv[4 * u] = v4.x;
+                wv[4 * u + 1] = v4.y;
+                wv[4 * u + 2] = v4.z;
+                wv[4 * u + 3] = v4.w;
+            }
             const uint32_t dq = tmem + TM_Q + C::QCOLS * static_cast<uint32_t>(n & 1) + lane_off;
 #pragma unroll
-            for (int h = 0; h < C::NH; ++h) {
-                uint32_t wv[32];
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    lds128(sQ + h * C::CHUNK + r * 128 + ((u ^ (r & 7)) << 4), wv[4 * u], wv[4 * u + 1], wv[4 * u + 2],
-                           wv[4 * u + 3]);
-                ptx::tmem_st32(dq + 32 * h, wv);
-            }
+            for (int hh = 0; hh < C::NH; ++hh)
+                ptx::tmem_st32(dq + 32 * hh, *reinterpret_cast<const uint32_t(*)[32]>(&wv[32 * hh]));
             ptx::tmem_wait_st();
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar_qt_full0 + 8 * static_cast<uint32_t>(n & 1));
-            ptx::mbar_arrive(bar_q_empty);
             if (r == 0) GNA_PROG(4, static_cast<int>(n) * 16 + 2);
         };
         Task t, tn;
         long long tau = next_task<BV>(p, blockIdx.x, ntask, t);
         long long n = 0;
-        if (tau >= 0) stage_q(0);
+        if (tau >= 0) stage_q(t, 0);
         for (; tau >= 0; ++n) {
             const long long tau_n = next_task<BV>(p, tau + gridDim.x, ntask, tn);
-            if (tau_n >= 0) stage_q(n + 1);
+            if (tau_n >= 0) stage_q(tn, n + 1);
             // ---- epilogue of task n
             int cc[3], x[3], bxo[3], inner;
             bool valid;
@@ -508,7 +562,7 @@ __global__ void __launch_bounds__(512, 1)
             t = tn;
         }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 160;\n" ::: "memory");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n" ::: "memory");
         // ========================================================== softmax
         const int h = warp >> 2;  // key half
         const int r = threadIdx.x & 127;
@@ -550,16 +604,23 @@ __global__ void __launch_bounds__(512, 1)
                 bool row_full = true;
                 int rlo[3], rhi[3];
                 if (!extra_stage) {
-                    int kc[KPB][3];
-                    bool dead[KPB];
+                    // the box holding this half's keys: box h of the stage (64-token boxes) or box 0
+                    int kc[3], kc1[3];
+                    bool dead, dead1;
+                    od.take(t, kc, dead);
+                    if (KPB == 2) {
+                        od.take(t, kc1, dead1);
+                        if (h) {
 #pragma unroll
-                    for (int u = 0; u < KPB; ++u) od.take(t, kc[u], dead[u]);
-                    const int u = KPB == 2 ? h : 0;  // the box holding this half's keys
+                            for (int a = 0; a < 3; ++a) kc[a] = kc1[a];
+                            dead = dead1;
+                        }
+                    }
 #pragma unroll
                     for (int a = 0; a < 3; ++a) {
-                        const int base = kc[u][a] * g.B[a];
+                        const int base = kc[a] * g.B[a];
                         rlo[a] = wst[a] - base;
-                        rhi[a] = dead[u] ? -1 : wen[a] - base;
+                        rhi[a] = dead ? -1 : wen[a] - base;
                         row_full = row_full && rlo[a] <= 0 && rhi[a] >= g.B[a];
                     }
                 }
@@ -568,7 +629,9 @@ __global__ void __launch_bounds__(512, 1)
                     extra_stage ? extra_left >= 64 : __all_sync(0xffffffffu, row_full || !valid);
 
                 if (r == 0) GNA_PROG(h * 2, static_cast<int>(ts) * 16 + 1);
+                if (r == 0 && h == 0) GT4(ts, 0);
                 ptx::mbar_wait(bar_s_full0 + 8 * b, static_cast<uint32_t>((ts >> 1) & 1));
+                if (r == 0) GT4(ts, 6 * h + 1);
                 if (r == 0) GNA_PROG(h * 2, static_cast<int>(ts) * 16 + 2);
                 if (j == 0 && r == 0 && h == 0) TL4(tau, 2);
                 ptx::tc_fence_after();
@@ -613,7 +676,9 @@ __global__ void __launch_bounds__(512, 1)
                 // ---- row max across the two key halves (warps w and w+4 own the same rows)
                 xm[(b * 2 + h) * 128 + r] = mloc;
                 if (r == 0) GNA_PROG(h * 2, static_cast<int>(ts) * 16 + 3);
+                if (r == 0 && h == 0) GT4(ts, 2);
                 named_bar_sync(1 + (warp & 3), 64);
+                if (r == 0 && h == 0) GT4(ts, 3);
                 if (r == 0) GNA_PROG(h * 2, static_cast<int>(ts) * 16 + 4);
                 const float mpart = xm[(b * 2 + (h ^ 1)) * 128 + r];
                 const float m_tile = fmaxf(mloc, mpart) * sl2;
@@ -658,10 +723,12 @@ __global__ void __launch_bounds__(512, 1)
                 }
                 l_run += (la0 + la1) + (lb0 + lb1);
                 if (r == 0) GNA_PROG(h * 2, static_cast<int>(ts) * 16 + 5);
+                if (r == 0 && h == 0) GT4(ts, 4);
                 ptx::tmem_st32(tS, pk);
                 ptx::tmem_wait_st();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(bar_p_full0 + 8 * (2 * b + h));
+                if (r == 0) GT4(ts, 6 * h + 5);
                 if (r == 0) GNA_PROG(h * 2, static_cast<int>(ts) * 16 + 6);
             }
             // ---- row statistics of the task for the epilogue warpgroup
@@ -728,6 +795,10 @@ cudaError_t launch_attention_v4(const AttnParams& p, const CUtensorMap& tq, cons
 extern "C" int gna_debug_timeline_v4(void* host, size_t bytes) {
     if (bytes > sizeof(gna::g_v4_tl)) bytes = sizeof(gna::g_v4_tl);
     return cudaMemcpyFromSymbol(host, gna::g_v4_tl, bytes) == cudaSuccess ? 0 : 3;
+}
+extern "C" int gna_debug_trace_v4(void* host, size_t bytes) {
+    if (bytes > sizeof(gna::g_v4_tr)) bytes = sizeof(gna::g_v4_tr);
+    return cudaMemcpyFromSymbol(host, gna::g_v4_tr, bytes) == cudaSuccess ? 0 : 3;
 }
 extern "C" int gna_debug_timeline_v4_reset(void) {
     static unsigned long long zeros[GNA_TL_CTAS * 8];

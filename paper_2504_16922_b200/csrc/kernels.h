@@ -22,6 +22,7 @@ struct AttnParams {
     int n_extra;            // extra (text) KV tokens per (batch, head), appended as dense stages
     int extra_stages;       // ceil(n_extra / 128)
     int* sched_counter;     // non-null: persistent kernel with a dynamic work queue (zeroed per launch)
+    const void* q_src;      // v4: Q rows read by the epilogue warpgroup (direct: user q; else permuted q)
     void* out_nat;          // if non-null: fused inverse permutation, O written to the user layout
     float* lse_nat;         //   and LSE likewise (may be null)
 };

@@ -111,6 +111,57 @@ __device__ __forceinline__ void tma_prefetch_2d(const void* desc, int c0, int c1
                  : "memory");
 }
 
+// 5-D tile prefetch into L2
+__device__ __forceinline__ void tma_prefetch_5d(const void* desc, int c0, int c1, int c2, int c3, int c4) {
+    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                     reinterpret_cast<uint64_t>(desc)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+                 : "memory");
+}
+
+// Warp-uniform TMA variants (every lane calls with identical operands, one elected lane issues)
+#define GNA_ELECT "elect.sync _|e, 0xffffffff;\n\t@e "
+__device__ __forceinline__ void mbar_expect_tx_e(uint32_t bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .pred e;\n\t" GNA_ELECT "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}" ::"r"(bar),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_e(uint32_t dst, const void* desc, uint32_t bar, int c0, int c1) {
+    asm volatile("{\n\t.reg .pred e;\n\t" GNA_ELECT
+                 "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3}], [%4];\n}" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_e(uint32_t dst, const void* desc, uint32_t bar, int c0, int c1, int c2) {
+    asm volatile("{\n\t.reg .pred e;\n\t" GNA_ELECT
+                 "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4}], [%5];\n}" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_5d_e(uint32_t dst, const void* desc, uint32_t bar, int c0, int c1, int c2,
+                                              int c3, int c4) {
+    asm volatile("{\n\t.reg .pred e;\n\t" GNA_ELECT
+                 "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n}" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(desc)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d_e(const void* desc, int c0, int c1) {
+    asm volatile("{\n\t.reg .pred e;\n\t" GNA_ELECT "cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n}" ::"l"(
+                     reinterpret_cast<uint64_t>(desc)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_5d_e(const void* desc, int c0, int c1, int c2, int c3, int c4) {
+    asm volatile("{\n\t.reg .pred e;\n\t" GNA_ELECT
+                 "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n}" ::"l"(
+                     reinterpret_cast<uint64_t>(desc)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+                 : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem),
@@ -148,6 +199,26 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Warp-uniform variants: every lane of the warp executes the call with identical operands and
+// one elected lane issues, so the compiler keeps operands in uniform registers (no per-MMA
+// election loop around a single-lane branch).
+__device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(bar)
         : "memory");
 }
 // mbarrier arrives once all previously issued tcgen05 ops of this thread completed

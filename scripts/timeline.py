@@ -26,7 +26,8 @@ for it in range(4):
     flush.zero_()
     lib.gna_debug_trace_reset()
     torch.cuda.synchronize()
-    gna.forward(q, k, v, f["window"], f["stride"], f["dilation"], f["causal"])
+    gna.forward(q, k, v, f["window"], f["stride"], f["dilation"], f["causal"],
+                flags=4 if os.environ.get("TRACE_PERMUTED") == "1" else 0)
     torch.cuda.synchronize()
 buf = np.zeros((8192, 8), dtype=np.uint64)
 assert lib.gna_debug_timeline(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
@@ -53,6 +54,11 @@ if V4:
     last = np.array([rel[sm == s_, 4].max() for s_ in np.unique(sm)])
     print(f"tasks per SM min {per_sm[per_sm>0].min()} max {per_sm.max()}; SM first start max {first.max():.1f} us; "
           f"SM end min {last.min():.1f} max {last.max():.1f} us")
+    ml = rel[:, 3] - rel[:, 2]
+    print("mainloop per task: p10 %.1f  median %.1f  p90 %.1f  max %.1f us" % tuple(np.percentile(ml, [10, 50, 90, 100])))
+    bysm = {int(s_): np.median(ml[sm == s_]) for s_ in np.unique(sm)}
+    v = np.array(sorted(bysm.values()))
+    print("per-SM median mainloop: min %.1f  median %.1f  max %.1f us" % (v.min(), np.median(v), v.max()))
     print("first task: setup->S0 %.2f us" % np.median(rel[np.argsort(rel[:, 0])[:148], 2] - rel[np.argsort(rel[:, 0])[:148], 0]))
     sys.exit(0)
 n = int((buf[:, 0] > 0).sum())

@@ -17,9 +17,30 @@ q, k, v = (t.cuda() for t in make_qkv(w.batch, w.spatial, w.heads, w.head_dim))
 lib = gna.load()
 for it in range(3):
     lib.gna_debug_trace_reset()
-    gna.forward(q, k, v, f["window"], f["stride"], f["dilation"], f["causal"])
+    gna.forward(q, k, v, f["window"], f["stride"], f["dilation"], f["causal"],
+                flags=4 if os.environ.get("TRACE_PERMUTED") == "1" else 0)
     torch.cuda.synchronize()
 buf = np.zeros((4, 256, 16), dtype=np.uint64)
+if os.environ.get("GNA_KERNEL", "v4") == "v4":
+    assert lib.gna_debug_trace_v4(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
+    names = ["smWait", "smS", "smXchg", "smExp", "smSt", "smP", "Sbeg", "h1S", "Sdone", "PVp0", "PVp1", "h1P",
+             "SKrdy", "PVbeg", "PVend", "prodK"]
+    for cta in range(2):
+        rows = buf[cta].astype(np.int64)
+        t0 = rows[rows > 0].min()
+        print(f"CTA {cta} (v4; cycles from the first event)")
+        print("  t  " + " ".join(f"{n:>7}" for n in names))
+        for t in range(256):
+            if rows[t].max() == 0:
+                break
+            if t < 24 or t % 10 == 0:
+                print(f"{t:3d}  " + " ".join(f"{int(x) - t0 if x else -1:7d}" for x in rows[t]))
+        v = rows[:, 1]
+        v = v[v > 0]
+        if len(v) > 10:
+            d = np.diff(v[4:])
+            print("  period (h0 S ready) median", int(np.median(d)))
+    sys.exit(0)
 assert lib.gna_debug_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
 names = {0: "S0rdy", 1: "S0ld", 2: "S0max", 3: "P0st", 4: "S1rdy", 5: "S1ld", 6: "S1max", 7: "P1st",
          8: "Vrdy", 9: "P0rdy", 10: "P1rdy", 11: "Knext", 12: "prodK", 13: "prodV"}
