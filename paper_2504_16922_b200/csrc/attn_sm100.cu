@@ -37,6 +37,19 @@
 
 #include "attn_common.cuh"
 
+#ifndef GNA_V3_ELECT
+#define GNA_V3_ELECT 1
+#endif
+#if GNA_V3_ELECT
+#define GNA_MMA_SS ptx::mma_ss_elect
+#define GNA_MMA_TS ptx::mma_ts_elect
+#define GNA_COMMIT ptx::mma_commit_elect
+#else
+#define GNA_MMA_SS ptx::mma_ss
+#define GNA_MMA_TS ptx::mma_ts
+#define GNA_COMMIT ptx::mma_commit
+#endif
+
 namespace gna {
 
 namespace {
@@ -208,7 +221,9 @@ __global__ void __launch_bounds__(384, 1)
         }
     } else if (warp == 9) {
         // ======================================================= MMA issuer
-        if (lane == 0) {
+        // warp-uniform: all lanes run the loop, one elected lane issues each tcgen05 op, so
+        // descriptors stay in uniform registers (GNA_V3_ELECT=0: lane 0 only, for A/B)
+        if (GNA_V3_ELECT || lane == 0) {
             constexpr uint32_t IDESC_QK = ptx::idesc_bf16(128, 128, 0, 0);
             constexpr uint32_t IDESC_PV = ptx::idesc_bf16(128, DP, 0, 1);
             const uint32_t tS0 = tmem, tS1 = tmem + 128;
@@ -219,7 +234,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int kk = 0; kk < DP / 16; ++kk) {
                     const uint32_t off = (kk >> 2) * C::CHUNK_BYTES + (kk & 3) * 32;
-                    ptx::mma_ss(i == 0 ? tS0 : tS1, ptx::smem_desc_sw128(qa + off, 16, 1024),
+                    GNA_MMA_SS(i == 0 ? tS0 : tS1, ptx::smem_desc_sw128(qa + off, 16, 1024),
                                 ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
                 }
             };
@@ -227,7 +242,7 @@ __global__ void __launch_bounds__(384, 1)
                 const uint32_t vb = sKV + slot * C::TILE_BYTES;
 #pragma unroll
                 for (int kk = k0; kk < k1; ++kk) {
-                    ptx::mma_ts(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + kk * 8,
+                    GNA_MMA_TS(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + kk * 8,
                                 ptx::smem_desc_sw128(vb + kk * 2048, C::CHUNK_BYTES, 1024), IDESC_PV,
                                 (acc || kk > 0) ? 1u : 0u);
                 }
@@ -239,16 +254,16 @@ __global__ void __launch_bounds__(384, 1)
             ++it;
             ptx::tc_fence_after();
             issue_qk(0, slotK);
-            ptx::mma_commit(bar_s_full0);
+            GNA_COMMIT(bar_s_full0);
             if (hasB) {
                 issue_qk(1, slotK);
-                ptx::mma_commit(bar_s_full0 + 8);
+                GNA_COMMIT(bar_s_full0 + 8);
             }
-            ptx::mma_commit(bar_kv_empty(slotK));
+            GNA_COMMIT(bar_kv_empty(slotK));
             for (int j = 0; j < nst; ++j) {
                 const int slotV = it % C::NS;
                 ptx::mbar_wait(bar_kv_full(slotV), (it / C::NS) & 1);
-                GT(j, 8);
+                if (lane == 0) GT(j, 8);
                 ++it;
                 const bool has_next = j + 1 < nst;
 #pragma unroll
@@ -258,17 +273,17 @@ __global__ void __launch_bounds__(384, 1)
                     issue_pv(0, slotV, j > 0 || c > 0, c * 8 / GNA_PSPLIT, (c + 1) * 8 / GNA_PSPLIT);
                 }
                 ptx::mbar_wait(bar_p_full0, j & 1);
-                GT(j, 9);
+                if (lane == 0) GT(j, 9);
                 ptx::tc_fence_after();
                 issue_pv(0, slotV, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * 8 / GNA_PSPLIT, 8);
                 if (has_next) {
                     slotK = it % C::NS;
                     ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
-                    GT(j, 11);
+                    if (lane == 0) GT(j, 11);
                     ++it;
                     ptx::tc_fence_after();
                     issue_qk(0, slotK);
-                    ptx::mma_commit(bar_s_full0);
+                    GNA_COMMIT(bar_s_full0);
                 }
                 if (hasB) {
 #pragma unroll
@@ -278,20 +293,20 @@ __global__ void __launch_bounds__(384, 1)
                         issue_pv(1, slotV, j > 0 || c > 0, c * 8 / GNA_PSPLIT, (c + 1) * 8 / GNA_PSPLIT);
                     }
                     ptx::mbar_wait(bar_p_full0 + 8, j & 1);
-                    GT(j, 10);
+                    if (lane == 0) GT(j, 10);
                     ptx::tc_fence_after();
                     issue_pv(1, slotV, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * 8 / GNA_PSPLIT, 8);
                 }
-                ptx::mma_commit(bar_kv_empty(slotV));
+                GNA_COMMIT(bar_kv_empty(slotV));
                 if (has_next) {
                     if (hasB) {
                         issue_qk(1, slotK);
-                        ptx::mma_commit(bar_s_full0 + 8);
+                        GNA_COMMIT(bar_s_full0 + 8);
                     }
-                    ptx::mma_commit(bar_kv_empty(slotK));
+                    GNA_COMMIT(bar_kv_empty(slotK));
                 }
             }
-            ptx::mma_commit(bar_o_full);
+            GNA_COMMIT(bar_o_full);
         }
       }
     } else {
