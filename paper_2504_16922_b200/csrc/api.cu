@@ -633,6 +633,25 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out_nat = fused_out ? a->out : nullptr;
     p.lse_nat = fused_out ? a->lse : nullptr;
+    // v3 epilogue: O through smem and TMA stores (GNA_TMA_STORE=0 keeps per-thread stores)
+    p.tma_store = 0;
+    const char* ts_env = getenv("GNA_TMA_STORE");
+    if (kc == 3 && !(ts_env && ts_env[0] == '0')) {
+        // The 5-D map folds batch into axis 0, so a box (or a padding box of the sub-tile grid)
+        // past the end of axis 0 would write into the next sample: only when the box grid tiles
+        // axis 0 exactly (or batch == 1).
+        // Dilated (strided) boxes keep the per-thread stores.
+        const bool dilated = c.g.ax[0].d > 1 || c.g.ax[1].d > 1 || c.g.ax[2].d > 1;
+        const bool tiles_axis0 = a->batch == 1 || c.g.nb[0] * c.g.B[0] == c.g.ax[0].L;  // no padded boxes
+        if (fused_out) {
+            bool ok = false;
+            if (!dilated && tiles_axis0 && (rc = make_tmap_direct(&p.tmap_o, a->out, c.g, &ok))) return rc;
+            p.tma_store = ok ? 2 : 0;
+        } else if (c.ws) {
+            if ((rc = make_tmap(&p.tmap_o, c.ws + c.L.o, c.g))) return rc;
+            p.tma_store = 1;
+        }
+    }
     if (kc == 4) GNA_CUDA_TRY(launch_attention_v4(p, tq, tk, tv, tek, tev, c.st));
     else GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, tek, tev, we - wb, c.st));
     return post_launch(a, c.st, "gna_attn_sm100");

@@ -500,6 +500,54 @@ __global__ void __launch_bounds__(384, 1)
             lrow = p.lse_perm + row_g;
             ncols = DP;
         }
+        if (p.tma_store) {
+            // O staged in this sub-tile's Q buffer (free: every QK^T has completed) in the
+            // SW128 layout of the Q tile, then TMA-stored box by box (coalesced; the 5-D map
+            // clips rows past the grid edges)
+            const uint32_t sO = sQ + i * C::TILE_BYTES;
+#pragma unroll
+            for (int c = 0; c < DP / 32; ++c) {
+                uint32_t rr[32];
+                ptx::tmem_ld32(tO + c * 32, rr);
+                ptx::tmem_wait_ld();
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    pk[e] = ptx::pack_bf16x2(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
+                const uint32_t rowb = sO + (c >> 1) * C::CHUNK_BYTES + r * 128;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    ptx::sts128(rowb + ((((c & 1) * 4 + q) ^ (r & 7)) << 4), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
+                                pk[4 * q + 3]);
+            }
+            ptx::fence_proxy_async_smem();
+            asm volatile("bar.sync %0, 128;" ::"r"(1 + i) : "memory");
+            if (r == 0) {
+                const long long b_idx = bh / g.heads;
+                const int h_idx = static_cast<int>(bh % g.heads);
+#pragma unroll
+                for (int u = 0; u < KPB; ++u) {
+                    const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
+                    const int k0 = sc[0] * g.QB[0] + u0, k1 = sc[1] * g.QB[1] + u1, k2 = sc[2] * g.QB[2] + u2;
+#pragma unroll
+                    for (int h = 0; h < C::NH; ++h) {
+                        const uint32_t src = sO + u * BV * 128 + h * C::CHUNK_BYTES;
+                        if (p.tma_store == 2) {
+                            const int c2 = cc[2] + g.ax[2].d * k2 * g.B[2];
+                            const int c3 = cc[1] + g.ax[1].d * k1 * g.B[1];
+                            const int c4 = static_cast<int>(b_idx * g.ax[0].L) + cc[0] + g.ax[0].d * k0 * g.B[0];
+                            ptx::tma_store_5d(&p.tmap_o, src, h * 64, h_idx, c2, c3, c4);
+                        } else {
+                            const int row =
+                                static_cast<int>(cls_row0 + static_cast<long long>((k0 * g.nb[1] + k1) * g.nb[2] + k2) * BV);
+                            ptx::tma_store_2d(&p.tmap_o, src, h * 64, row);
+                        }
+                    }
+                }
+                ptx::bulk_commit();
+                ptx::bulk_wait_read0();
+            }
+        } else {
 #pragma unroll
         for (int c = 0; c < DP / 32; ++c) {
             uint32_t rr[32];
@@ -514,6 +562,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             }
+        }
         }
         if (valid && lrow != nullptr) {
             const float m_eff = m_used == -INFINITY ? 0.f : m_used;

@@ -25,6 +25,10 @@ struct AttnParams {
     const void* q_src;      // v4: Q rows read by the epilogue warpgroup (direct: user q; else permuted q)
     void* out_nat;          // if non-null: fused inverse permutation, O written to the user layout
     float* lse_nat;         //   and LSE likewise (may be null)
+    // O written by TMA stores from smem (v3): 0 = per-thread stores, 1 = 2-D map over the
+    // permuted O rows, 2 = 5-D map over the user's O [B][s0][s1][s2][H][D] (clips padding)
+    int tma_store;
+    CUtensorMap tmap_o;
 };
 
 // Permuted layout sizes (rows of Dp elements)

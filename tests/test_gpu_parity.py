@@ -301,3 +301,26 @@ def test_degenerate_shapes(gna, cfg):
     (q, k, v), o, l = _run(gna, cfg, B, H, D, True)
     ro, rl = O.forward(as_f32_numpy(q), as_f32_numpy(k), as_f32_numpy(v), O.Params(**cfg))
     _assert_close(o, ro, l, rl)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [SMALL[2], SMALL[5], SMALL[6], SMALL[3]], ids=_ids)
+def test_tma_store_epilogue_bitwise(gna, cfg, monkeypatch):
+    """The epilogue's smem + TMA-store route writes exactly what the per-thread stores write
+    (same values, no spill into the neighbouring sample or padding rows), on the direct and the
+    permuted stage path; GNA_TMA_STORE=0 selects the per-thread stores."""
+    B, H, D = 2, 2, 128
+    q, k, v = (t.cuda() for t in make_qkv(B, cfg["spatial"], H, D, discriminating=True))
+    res = {}
+    for ts in ("0", "1"):
+        monkeypatch.setenv("GNA_TMA_STORE", ts)
+        o, l = gna.forward(q, k, v, cfg["window"], cfg["stride"], cfg.get("dilation"), cfg.get("causal"))
+        o2 = torch.empty_like(q)
+        l2 = torch.empty_like(l)
+        gna.permute(q, k, v, o2, cfg["window"], cfg["stride"], cfg.get("dilation"), cfg.get("causal"))
+        gna.attention_permuted(q, k, v, o2, cfg["window"], cfg["stride"], cfg.get("dilation"), cfg.get("causal"))
+        gna.unpermute(q, k, v, o2, l2, cfg["window"], cfg["stride"], cfg.get("dilation"), cfg.get("causal"))
+        torch.cuda.synchronize()
+        res[ts] = (o, l, o2, l2)
+    for a, b in zip(res["0"], res["1"]):
+        assert torch.equal(a, b)
