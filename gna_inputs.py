@@ -116,3 +116,14 @@ def sample_rows(batch, spatial, heads, n_uniform, seed=SEED + 99, extra_tokens=(
     if ext:
         rows = np.concatenate([rows, np.asarray(ext, dtype=np.int64)], axis=0)
     return np.ascontiguousarray(rows, dtype=np.int64)
+
+
+def quantize_e4m3(t: torch.Tensor):
+    """Per-tensor E4M3 quantisation of an input tensor (SURVEY NEXT-3 inputs): scale =
+    amax / 448 (E4M3's largest finite value), values rounded to nearest by torch's cast.
+    Returns (e4m3 tensor, scale, dequantised fp32 tensor = e4m3 * scale) -- the exact values
+    the FP8 kernel consumes, which is what the oracle is run on."""
+    x = t.to(torch.float32)
+    scale = float(x.abs().max().clamp_min(1e-30)) / 448.0
+    t8 = (x / scale).to(torch.float8_e4m3fn)
+    return t8, scale, t8.to(torch.float32) * scale

@@ -76,6 +76,14 @@ extern "C" {
 #define GNA_ENOMEM 4
 
 #define GNA_DTYPE_BF16 0
+/* E4M3 Q/K/V with per-tensor scales (gna_args.q_scale/k_scale/v_scale: real value =
+ * stored value x scale), bf16 O and fp32 LSE -- the FP8 forward the paper quotes for its
+ * Blackwell kernel.  QK^T and PV run as E4M3
+ * tcgen05 MMAs (kind::f8f6f4, fp32 accumulation); P is rounded to E4M3 (RNE, saturating)
+ * before PV, the softmax and row sums stay fp32.  head_dim 128, no extra KV tokens, and
+ * only the permute-free path (gna_forward / gna_forward_ex); the stage API returns
+ * GNA_EUNSUPPORTED for it. */
+#define GNA_DTYPE_FP8_E4M3 2
 
 /* flags */
 #define GNA_FLAG_SYNC_CHECK 1        /* synchronize + check after each launch (debug) */
@@ -92,7 +100,7 @@ typedef struct gna_args {
     int batch, heads, head_dim;
     int spatial[3], window[3], stride[3], dilation[3], causal[3];
     float scale;            /* <= 0 -> 1/sqrt(head_dim) */
-    int dtype;              /* GNA_DTYPE_BF16 */
+    int dtype;              /* GNA_DTYPE_BF16 or GNA_DTYPE_FP8_E4M3 (q, k, v; out stays bf16) */
     void *stream;           /* cudaStream_t */
     void *workspace;        /* optional caller workspace (device, 256-B aligned) */
     size_t workspace_bytes;
@@ -107,6 +115,8 @@ typedef struct gna_args {
      * neighbourhood.  0 / NULL = none.  Requires head_dim >= 64. */
     const void *extra_k, *extra_v;
     int n_extra;
+    /* GNA_DTYPE_FP8_E4M3 only: per-tensor dequantisation scales (<= 0 -> 1). */
+    float q_scale, k_scale, v_scale;
 } gna_args;
 
 /* Plan summary for a problem (host struct, filled by gna_plan_info). */

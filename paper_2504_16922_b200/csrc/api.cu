@@ -61,7 +61,14 @@ int pow2ceil(int x) { return 1 << ilog2(x < 1 ? 1 : x); }
 // --------------------------------------------------------------- validation
 int validate(const gna_args* a, bool need_ptrs) {
     if (!a) return fail(GNA_EINVAL, "args is NULL");
-    if (a->dtype != GNA_DTYPE_BF16) return fail(GNA_EUNSUPPORTED, "dtype: only GNA_DTYPE_BF16 is supported");
+    if (a->dtype != GNA_DTYPE_BF16 && a->dtype != GNA_DTYPE_FP8_E4M3)
+        return fail(GNA_EUNSUPPORTED, "dtype: GNA_DTYPE_BF16 or GNA_DTYPE_FP8_E4M3");
+    if (a->dtype == GNA_DTYPE_FP8_E4M3) {
+        if (a->head_dim != 128) return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 needs head_dim 128");
+        if (a->n_extra > 0) return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 with extra KV tokens is not supported");
+        if (!(a->q_scale >= 0.f && a->k_scale >= 0.f && a->v_scale >= 0.f))
+            return fail(GNA_EINVAL, "q_scale/k_scale/v_scale must be >= 0 (0 = 1)");
+    }
     if (a->batch < 1) return fail(GNA_EINVAL, "batch must be >= 1");
     if (a->heads < 1) return fail(GNA_EINVAL, "heads must be >= 1");
     if (a->head_dim != 32 && a->head_dim != 64 && a->head_dim != 128)
@@ -498,24 +505,25 @@ int make_tmap(CUtensorMap* m, const void* base, const Geometry& g) {
 // 5-D map over a user tensor [B][s0][s1][s2][H][D] (direct, permute-free mode):
 // dims (D, H, s2, s1, B*s0), box {64, 1, B2*d2, B1*d1, B0*d0}, element strides
 // (1, 1, d2, d1, d0): one box load gathers the box of one dilation class of one head.
-int make_tmap_direct(CUtensorMap* m, const void* base, const Geometry& g, bool* ok) {
+int make_tmap_direct(CUtensorMap* m, const void* base, const Geometry& g, bool* ok, int elem_bytes = 2) {
     *ok = false;
     EncodeTiledFn enc = get_encode();
     if (!enc) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled unavailable");
     if (g.D < 64) return GNA_OK;
     for (int a = 0; a < 3; ++a)
         if (g.B[a] * g.ax[a].d > 256 || g.ax[a].d > 8) return GNA_OK;
-    const cuuint64_t D = g.D, H = g.heads;
+    const cuuint64_t D = g.D, H = g.heads, E = static_cast<cuuint64_t>(elem_bytes);
     cuuint64_t dims[5] = {D, H, static_cast<cuuint64_t>(g.ax[2].L), static_cast<cuuint64_t>(g.ax[1].L),
                           static_cast<cuuint64_t>(g.batch) * g.ax[0].L};
-    cuuint64_t strides[4] = {D * 2, H * D * 2, g.ax[2].L * H * D * 2,
-                             static_cast<cuuint64_t>(g.ax[1].L) * g.ax[2].L * H * D * 2};
-    cuuint32_t box[5] = {64, 1, static_cast<cuuint32_t>(g.B[2] * g.ax[2].d), static_cast<cuuint32_t>(g.B[1] * g.ax[1].d),
+    cuuint64_t strides[4] = {D * E, H * D * E, g.ax[2].L * H * D * E,
+                             static_cast<cuuint64_t>(g.ax[1].L) * g.ax[2].L * H * D * E};
+    cuuint32_t box[5] = {static_cast<cuuint32_t>(128 / elem_bytes), 1, static_cast<cuuint32_t>(g.B[2] * g.ax[2].d), static_cast<cuuint32_t>(g.B[1] * g.ax[1].d),
                          static_cast<cuuint32_t>(g.B[0] * g.ax[0].d)};
     cuuint32_t estr[5] = {1, 1, static_cast<cuuint32_t>(g.ax[2].d), static_cast<cuuint32_t>(g.ax[1].d),
                           static_cast<cuuint32_t>(g.ax[0].d)};
     if (dims[4] >= (1ull << 31)) return GNA_OK;
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box, estr,
+    CUresult r = enc(m, elem_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+                     const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     *ok = r == CUDA_SUCCESS;
@@ -614,7 +622,8 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.n_extra = a->n_extra > 0 ? a->n_extra : 0;
     p.extra_stages = (p.n_extra + 127) / 128;
     p.sched_counter = nullptr;
-    const int kc = kernel_choice();
+    const bool fp8 = a->dtype == GNA_DTYPE_FP8_E4M3;
+    const int kc = fp8 ? 3 : kernel_choice();  // the E4M3 path exists in the v3 kernel only
     if ((kc == 2 || (kc == 3 && use_persistent())) && (rc = next_counter(&p.sched_counter))) return rc;
     p.g = c.g;
     p.items = items;
@@ -631,6 +640,12 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.lse_perm = c.ws ? reinterpret_cast<float*>(c.ws + c.L.lse) : nullptr;
     const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));
     p.scale_log2 = scale * 1.4426950408889634f;
+    p.fp8 = fp8 ? 1 : 0;
+    p.o_scale = 1.0f;
+    if (fp8) {  // per-tensor dequantisation: S scales by q_scale*k_scale, O by v_scale
+        p.scale_log2 *= (a->q_scale > 0.f ? a->q_scale : 1.f) * (a->k_scale > 0.f ? a->k_scale : 1.f);
+        p.o_scale = a->v_scale > 0.f ? a->v_scale : 1.f;
+    }
     p.out_nat = fused_out ? a->out : nullptr;
     p.lse_nat = fused_out ? a->lse : nullptr;
     // v3 epilogue: O through smem and TMA stores (GNA_TMA_STORE=0 keeps per-thread stores)
@@ -674,15 +689,18 @@ int gna_forward_ex(const gna_args* a) {
     Ctx c;
     int rc = prepare(a, true, &c, /*need_ws=*/false);
     if (rc) return rc;
-    if (!(a->flags & (GNA_FLAG_PERMUTED | GNA_FLAG_UNFUSED_EPILOGUE))) {
+    const bool fp8 = a->dtype == GNA_DTYPE_FP8_E4M3;
+    if (fp8 || !(a->flags & (GNA_FLAG_PERMUTED | GNA_FLAG_UNFUSED_EPILOGUE))) {
         // permute-free path: one kernel, 5-D TMA boxes straight from the user tensors,
         // O and LSE scattered by the epilogue
         CUtensorMap maps[3];
         bool ok[3];
-        if ((rc = make_tmap_direct(&maps[0], a->q, c.g, &ok[0]))) return rc;
-        if ((rc = make_tmap_direct(&maps[1], a->k, c.g, &ok[1]))) return rc;
-        if ((rc = make_tmap_direct(&maps[2], a->v, c.g, &ok[2]))) return rc;
+        const int eb = fp8 ? 1 : 2;
+        if ((rc = make_tmap_direct(&maps[0], a->q, c.g, &ok[0], eb))) return rc;
+        if ((rc = make_tmap_direct(&maps[1], a->k, c.g, &ok[1], eb))) return rc;
+        if ((rc = make_tmap_direct(&maps[2], a->v, c.g, &ok[2], eb))) return rc;
         if (ok[0] && ok[1] && ok[2]) return do_attention(a, c, /*fused_out=*/true, /*direct=*/true, maps);
+        if (fp8) return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 needs the permute-free path (box*dilation <= 256, dilation <= 8)");
     }
     if ((rc = get_workspace(a, c.L.total, &c.ws))) return rc;
     if ((rc = do_permute(a, c))) return rc;
@@ -720,6 +738,8 @@ int gna_forward(const void* q, const void* k, const void* v, void* out, float* l
 }
 
 int gna_permute(const gna_args* a) {
+    if (a && a->dtype == GNA_DTYPE_FP8_E4M3)
+        return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 runs on the permute-free path only (gna_forward_ex)");
     if (!a || !a->q || !a->k || !a->v) return fail(GNA_EINVAL, "q/k/v NULL");
     Ctx c;
     int rc = prepare(a, false, &c);
@@ -728,6 +748,8 @@ int gna_permute(const gna_args* a) {
 }
 
 int gna_attention_permuted(const gna_args* a) {
+    if (a && a->dtype == GNA_DTYPE_FP8_E4M3)
+        return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 runs on the permute-free path only (gna_forward_ex)");
     Ctx c;
     int rc = prepare(a, false, &c);
     if (rc) return rc;
@@ -735,6 +757,8 @@ int gna_attention_permuted(const gna_args* a) {
 }
 
 int gna_unpermute(const gna_args* a) {
+    if (a && a->dtype == GNA_DTYPE_FP8_E4M3)
+        return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 runs on the permute-free path only (gna_forward_ex)");
     if (!a || !a->out) return fail(GNA_EINVAL, "out NULL");
     Ctx c;
     int rc = prepare(a, false, &c);

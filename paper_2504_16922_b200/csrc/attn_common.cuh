@@ -65,13 +65,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
 namespace gna {
 namespace attn {
 
-template <int DP, int BV>
+template <int DP, int BV, bool F8 = false>
 struct Cfg {
-    static constexpr int NH = DP / 64;               // 128-byte column chunks ("halves")
+    // bf16: DP/64 column chunks of 128 B per row; E4M3 (F8): one 128-B chunk holds 128 elements
+    static constexpr int NH = F8 ? 1 : DP / 64;      // 128-byte column chunks ("halves") of Q/K/V
+    static constexpr int ONH = DP / 64;              // 128-byte chunks of a bf16 O row
     static constexpr int CHUNK_BYTES = 128 * 128;    // 128 rows x 128 B, one SW128 chunk
-    static constexpr int TILE_BYTES = NH * CHUNK_BYTES;  // 128 rows x DP bf16
-    static constexpr int NS = DP == 128 ? GNA_NS128 : 8;  // KV ring slots (K and V share it)
+    static constexpr int TILE_BYTES = NH * CHUNK_BYTES;  // 128 rows x DP elements
+    static constexpr int NS = F8 ? 8 : (DP == 128 ? GNA_NS128 : 8);  // KV ring slots (K and V share it)
     static constexpr int KPB = 128 / BV;             // boxes per 128-row tile
+    static constexpr int KSTEP = F8 ? 32 : 16;       // MMA K per instruction
     static constexpr int Q_OFF = 0;
     static constexpr int KV_OFF = 2 * TILE_BYTES;
     static constexpr int BAR_OFF = KV_OFF + NS * TILE_BYTES;

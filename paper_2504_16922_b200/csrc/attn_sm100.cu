@@ -56,13 +56,14 @@ namespace {
 using namespace attn;
 }  // namespace
 
-template <int DP, int BV>
+template <int DP, int BV, bool F8>
 __global__ void __launch_bounds__(384, 1)
     gna_attn_sm100(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                    const __grid_constant__ CUtensorMap tmap_ek, const __grid_constant__ CUtensorMap tmap_ev) {
-    using C = Cfg<DP, BV>;
+    using C = Cfg<DP, BV, F8>;
     constexpr int KPB = C::KPB;
+    static_assert(!F8 || (DP == 128 && GNA_PSPLIT <= 2), "E4M3 path: head_dim 128, P split 1 or 2");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* sgen = smem_raw + (sbase - ptx::smem_u32(smem_raw));
@@ -224,27 +225,39 @@ __global__ void __launch_bounds__(384, 1)
         // warp-uniform: all lanes run the loop, one elected lane issues each tcgen05 op, so
         // descriptors stay in uniform registers (GNA_V3_ELECT=0: lane 0 only, for A/B)
         if (GNA_V3_ELECT || lane == 0) {
-            constexpr uint32_t IDESC_QK = ptx::idesc_bf16(128, 128, 0, 0);
-            constexpr uint32_t IDESC_PV = ptx::idesc_bf16(128, DP, 0, 1);
+            constexpr uint32_t IDESC_QK = F8 ? ptx::idesc_e4m3(128, 128, 0, 0) : ptx::idesc_bf16(128, 128, 0, 0);
+            constexpr uint32_t IDESC_PV = F8 ? ptx::idesc_e4m3(128, DP, 0, 1) : ptx::idesc_bf16(128, DP, 0, 1);
+            constexpr int KQ = DP / C::KSTEP;   // QK^T instructions (K = head_dim)
+            constexpr int KP = 128 / C::KSTEP;  // PV instructions (K = 128 keys); P step = 8 TMEM columns
+            constexpr uint32_t V_STEP = C::KSTEP * 128;  // bytes of V per K step (rows of 128 B)
             const uint32_t tS0 = tmem, tS1 = tmem + 128;
             const uint32_t tO0 = tmem + 256, tO1 = tmem + 384;
             auto issue_qk = [&](int i, int slot) {
                 const uint32_t qa = sQ + i * C::TILE_BYTES;
                 const uint32_t kb = sKV + slot * C::TILE_BYTES;
 #pragma unroll
-                for (int kk = 0; kk < DP / 16; ++kk) {
+                for (int kk = 0; kk < KQ; ++kk) {
                     const uint32_t off = (kk >> 2) * C::CHUNK_BYTES + (kk & 3) * 32;
-                    GNA_MMA_SS(i == 0 ? tS0 : tS1, ptx::smem_desc_sw128(qa + off, 16, 1024),
-                                ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
+                    if constexpr (F8)
+                        ptx::mma_ss_f8_elect(i == 0 ? tS0 : tS1, ptx::smem_desc_sw128(qa + off, 16, 1024),
+                                             ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
+                    else
+                        GNA_MMA_SS(i == 0 ? tS0 : tS1, ptx::smem_desc_sw128(qa + off, 16, 1024),
+                                   ptx::smem_desc_sw128(kb + off, 16, 1024), IDESC_QK, kk > 0);
                 }
             };
-            auto issue_pv = [&](int i, int slot, bool acc, int k0 = 0, int k1 = 8) {
+            auto issue_pv = [&](int i, int slot, bool acc, int k0, int k1) {
                 const uint32_t vb = sKV + slot * C::TILE_BYTES;
 #pragma unroll
                 for (int kk = k0; kk < k1; ++kk) {
-                    GNA_MMA_TS(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + kk * 8,
-                                ptx::smem_desc_sw128(vb + kk * 2048, C::CHUNK_BYTES, 1024), IDESC_PV,
-                                (acc || kk > 0) ? 1u : 0u);
+                    if constexpr (F8)
+                        ptx::mma_ts_f8_elect(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + kk * 8,
+                                             ptx::smem_desc_sw128(vb + kk * V_STEP, C::CHUNK_BYTES, 1024), IDESC_PV,
+                                             (acc || kk > 0) ? 1u : 0u);
+                    else
+                        GNA_MMA_TS(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + kk * 8,
+                                   ptx::smem_desc_sw128(vb + kk * V_STEP, C::CHUNK_BYTES, 1024), IDESC_PV,
+                                   (acc || kk > 0) ? 1u : 0u);
                 }
             };
             ptx::mbar_wait(bar_q, 0);
@@ -270,12 +283,12 @@ __global__ void __launch_bounds__(384, 1)
                 for (int c = 0; c < GNA_PSPLIT - 1; ++c) {
                     ptx::mbar_wait(bar_pc0 + 8 * c, j & 1);
                     ptx::tc_fence_after();
-                    issue_pv(0, slotV, j > 0 || c > 0, c * 8 / GNA_PSPLIT, (c + 1) * 8 / GNA_PSPLIT);
+                    issue_pv(0, slotV, j > 0 || c > 0, c * KP / GNA_PSPLIT, (c + 1) * KP / GNA_PSPLIT);
                 }
                 ptx::mbar_wait(bar_p_full0, j & 1);
                 if (lane == 0) GT(j, 9);
                 ptx::tc_fence_after();
-                issue_pv(0, slotV, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * 8 / GNA_PSPLIT, 8);
+                issue_pv(0, slotV, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * KP / GNA_PSPLIT, KP);
                 if (has_next) {
                     slotK = it % C::NS;
                     ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
@@ -290,12 +303,12 @@ __global__ void __launch_bounds__(384, 1)
                     for (int c = 0; c < GNA_PSPLIT - 1; ++c) {
                         ptx::mbar_wait(bar_pc0 + 8 * (3 + c), j & 1);
                         ptx::tc_fence_after();
-                        issue_pv(1, slotV, j > 0 || c > 0, c * 8 / GNA_PSPLIT, (c + 1) * 8 / GNA_PSPLIT);
+                        issue_pv(1, slotV, j > 0 || c > 0, c * KP / GNA_PSPLIT, (c + 1) * KP / GNA_PSPLIT);
                     }
                     ptx::mbar_wait(bar_p_full0 + 8, j & 1);
                     if (lane == 0) GT(j, 10);
                     ptx::tc_fence_after();
-                    issue_pv(1, slotV, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * 8 / GNA_PSPLIT, 8);
+                    issue_pv(1, slotV, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * KP / GNA_PSPLIT, KP);
                 }
                 GNA_COMMIT(bar_kv_empty(slotV));
                 if (has_next) {
@@ -447,13 +460,23 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
                 else ptx::fadd2(la0, la1, la0, la1, y0, y1);
-                pk[pi] = ptx::pack_bf16x2(y0, y1);
-                constexpr int CH = 64 / GNA_PSPLIT;  // packed P columns per chunk
+                constexpr int CH = 64 / GNA_PSPLIT;  // key pairs per P chunk
+                if constexpr (F8) {
+                    // E4M3 P (P <= 2^8 by the lazy max, inside E4M3's range): 4 keys per TMEM column
+                    const uint32_t h16 = ptx::pack_e4m3x2(y0, y1);
+                    if (pi & 1) pk[pi >> 1] |= h16 << 16;
+                    else pk[pi >> 1] = h16;
+                } else {
+                    pk[pi] = ptx::pack_bf16x2(y0, y1);
+                }
                 if (pi % CH == CH - 1) {
                     // P columns of this chunk (keys [2*(pi+1-CH), 2*(pi+1))) are final: store them and,
                     // except for the last chunk, let the MMA start the PV on them right away
                     const int c0 = pi + 1 - CH;
-                    if (CH == 32) ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
+                    if constexpr (F8) {
+                        if (CH == 64) ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
+                        else ptx::tmem_st16(tS + c0 / 2, &pk[c0 / 2]);
+                    } else if (CH == 32) ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
                     else if (CH == 16) ptx::tmem_st16(tS + c0, &pk[c0]);
                     else {
                         ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
@@ -477,7 +500,7 @@ __global__ void __launch_bounds__(384, 1)
         // ---------------------------------------------------------- epilogue
         ptx::mbar_wait(bar_o_full, 0);
         ptx::tc_fence_after();
-        const float inv_l = l_run > 0.f ? 1.0f / l_run : 0.f;
+        const float inv_l = (l_run > 0.f ? 1.0f / l_run : 0.f) * p.o_scale;
         // Output row: the permuted O row (stage API), or -- fused inverse permutation
         // -- the row of this token in the user's heads-last
         // layout [B][s0][s1][s2][H][D], so no separate unpermute pass is needed.
@@ -504,7 +527,9 @@ __global__ void __launch_bounds__(384, 1)
             // O staged in this sub-tile's Q buffer (free: every QK^T has completed) in the
             // SW128 layout of the Q tile, then TMA-stored box by box (coalesced; the 5-D map
             // clips rows past the grid edges)
-            const uint32_t sO = sQ + i * C::TILE_BYTES;
+            // bf16: this sub-tile's Q buffer; E4M3: Q tiles are half the size of a bf16 O tile,
+            // the K/V ring (drained: every MMA has completed) holds it instead
+            const uint32_t sO = F8 ? sKV + i * 2 * C::CHUNK_BYTES : sQ + i * C::TILE_BYTES;
 #pragma unroll
             for (int c = 0; c < DP / 32; ++c) {
                 uint32_t rr[32];
@@ -530,7 +555,7 @@ __global__ void __launch_bounds__(384, 1)
                     const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
                     const int k0 = sc[0] * g.QB[0] + u0, k1 = sc[1] * g.QB[1] + u1, k2 = sc[2] * g.QB[2] + u2;
 #pragma unroll
-                    for (int h = 0; h < C::NH; ++h) {
+                    for (int h = 0; h < C::ONH; ++h) {
                         const uint32_t src = sO + u * BV * 128 + h * C::CHUNK_BYTES;
                         if (p.tma_store == 2) {
                             const int c2 = cc[2] + g.ax[2].d * k2 * g.B[2];
@@ -584,20 +609,20 @@ __global__ void __launch_bounds__(384, 1)
 
 #include "attn_persistent.cuh"
 
-template <int DP, int BV>
+template <int DP, int BV, bool F8 = false>
 static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
                             cudaStream_t stream) {
-    using C = Cfg<DP, BV>;
+    using C = Cfg<DP, BV, F8>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gna_attn_sm100<DP, BV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(gna_attn_sm100<DP, BV, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     if (n_ctas <= 0) return cudaSuccess;
-    if (p.sched_counter != nullptr) {
+    if constexpr (!F8) if (p.sched_counter != nullptr) {
         static bool pconfigured = false;
         if (!pconfigured) {
             cudaError_t e = cudaFuncSetAttribute(gna_attn_sm100_persistent<DP, BV>,
@@ -619,7 +644,7 @@ static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CU
             <<<static_cast<unsigned>(grid), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
         return cudaGetLastError();
     }
-    gna_attn_sm100<DP, BV><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
+    gna_attn_sm100<DP, BV, F8><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
     return cudaGetLastError();
 }
 
@@ -627,6 +652,12 @@ cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const C
                              const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
                              cudaStream_t stream) {
     const int dp = p.g.Dp, bv = p.g.box_vol;
+    if (p.fp8) {
+        if (p.sched_counter != nullptr || dp != 128) return cudaErrorInvalidValue;
+        if (bv == 128) return launch_t<128, 128, true>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+        if (bv == 64) return launch_t<128, 64, true>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+        return cudaErrorInvalidValue;
+    }
     if (dp == 128 && bv == 128) return launch_t<128, 128>(p, tq, tk, tv, tek, tev, n_ctas, stream);
     if (dp == 128 && bv == 64) return launch_t<128, 64>(p, tq, tk, tv, tek, tev, n_ctas, stream);
     if (dp == 64 && bv == 128) return launch_t<64, 128>(p, tq, tk, tv, tek, tev, n_ctas, stream);

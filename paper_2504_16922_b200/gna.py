@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("GNA_LIB_PATH") or os.path.join(_HERE, "libgna_b200.so
 
 GNA_OK, GNA_EINVAL, GNA_EUNSUPPORTED, GNA_ECUDA, GNA_ENOMEM = range(5)
 GNA_DTYPE_BF16 = 0
+GNA_DTYPE_FP8_E4M3 = 2
 GNA_FLAG_SYNC_CHECK = 1
 GNA_FLAG_UNFUSED_EPILOGUE = 2
 GNA_FLAG_PERMUTED = 4
@@ -36,6 +37,7 @@ class GnaArgs(ctypes.Structure):
         ("box", _I3), ("work_begin", ctypes.c_longlong), ("work_end", ctypes.c_longlong),
         ("flags", ctypes.c_int),
         ("extra_k", ctypes.c_void_p), ("extra_v", ctypes.c_void_p), ("n_extra", ctypes.c_int),
+        ("q_scale", ctypes.c_float), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float),
     ]
 
 
@@ -100,7 +102,7 @@ def _pad3(x, fill):
 def make_args(batch, heads, head_dim, spatial, window, stride=None, dilation=None, causal=None,
               scale=0.0, q=None, k=None, v=None, out=None, lse=None, stream=None, box=None,
               work_range=None, workspace=None, workspace_bytes=0, flags=0, extra_k=None, extra_v=None,
-              n_extra=0) -> GnaArgs:
+              n_extra=0, dtype=GNA_DTYPE_BF16, scales=(0.0, 0.0, 0.0)) -> GnaArgs:
     n = len(spatial)
     a = GnaArgs()
     a.q, a.k, a.v, a.out, a.lse = q, k, v, out, lse
@@ -111,7 +113,8 @@ def make_args(batch, heads, head_dim, spatial, window, stride=None, dilation=Non
     a.dilation = _I3(*_pad3(dilation if dilation is not None else [1] * n, 1))
     a.causal = _I3(*[int(bool(c)) for c in _pad3(causal if causal is not None else [0] * n, 0)])
     a.scale = float(scale or 0.0)
-    a.dtype = GNA_DTYPE_BF16
+    a.dtype = int(dtype)
+    a.q_scale, a.k_scale, a.v_scale = (float(x) for x in scales)
     a.stream = stream
     a.workspace = workspace
     a.workspace_bytes = int(workspace_bytes)
@@ -123,14 +126,16 @@ def make_args(batch, heads, head_dim, spatial, window, stride=None, dilation=Non
 
 
 def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,
-                 workspace=None, extra_k=None, extra_v=None):
+                 workspace=None, extra_k=None, extra_v=None, scales=None):
     import torch
 
+    fp8 = q.dtype == torch.float8_e4m3fn
     for name, t in (("q", q), ("k", k), ("v", v), ("out", out)):
         if not t.is_cuda:
             raise GnaError(f"{name} must be a CUDA tensor (no CPU fallback)")
-        if t.dtype != torch.bfloat16:
-            raise GnaError(f"{name} must be bfloat16")
+        want = torch.float8_e4m3fn if (fp8 and name != "out") else torch.bfloat16
+        if t.dtype != want:
+            raise GnaError(f"{name} must be {want} (q, k, v all bfloat16, or all float8_e4m3fn with a bfloat16 out)")
         if not t.is_contiguous():
             raise GnaError(f"{name} must be contiguous")
     if lse is not None and (lse.dtype != torch.float32 or not lse.is_contiguous()):
@@ -158,24 +163,28 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
                      q=q.data_ptr(), k=k.data_ptr(), v=v.data_ptr(), out=out.data_ptr(),
                      lse=(lse.data_ptr() if lse is not None else None), stream=stream, box=box,
                      work_range=work_range, flags=flags, workspace=ws_ptr, workspace_bytes=ws_bytes,
-                     extra_k=ek, extra_v=ev, n_extra=n_extra)
+                     extra_k=ek, extra_v=ev, n_extra=n_extra,
+                     dtype=GNA_DTYPE_FP8_E4M3 if fp8 else GNA_DTYPE_BF16,
+                     scales=tuple(scales) if scales is not None else (0.0, 0.0, 0.0))
 
 
 def forward(q, k, v, window, stride=None, dilation=None, causal=None, scale=None, out=None, lse=None,
             box=None, work_range=None, stream=None, return_lse=True, flags=0, workspace=None, extra_k=None,
-            extra_v=None):
+            extra_v=None, scales=None):
     """GNA forward on CUDA bf16 tensors [B, *spatial, H, D] (heads-last); optional extra
-    (text) keys/values [B, T, H, D] attended densely by every query.
+    (text) keys/values [B, T, H, D] attended densely by every query.  q, k, v may instead be
+    torch.float8_e4m3fn with per-tensor dequantisation scales=(q_scale, k_scale, v_scale)
+    (GNA_DTYPE_FP8_E4M3, head_dim 128); out stays bfloat16.
 
     Returns (out, lse) -- lse fp32 [B, *spatial, H] (natural log)."""
     import torch
 
     if out is None:
-        out = torch.empty_like(q)
+        out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
     if lse is None and return_lse:
         lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
     a = _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,
-                     workspace, extra_k, extra_v)
+                     workspace, extra_k, extra_v, scales)
     with torch.cuda.device(q.device):
         _check(load().gna_forward_ex(ctypes.byref(a)))
     return out, lse

@@ -156,3 +156,16 @@ def test_extra_tokens_validation(gna):
         gna.plan_info(1, 1, 32, (64,), (8,), n_extra=4)
     with pytest.raises(GnaError, match="n_extra"):
         gna.plan_info(1, 1, 64, (64,), (8,), n_extra=-1)
+
+
+def test_fp8_validation_without_gpu():
+    """GNA_DTYPE_FP8_E4M3 argument checks run before any device access (nothing launched)."""
+    import ctypes
+    import paper_2504_16922_b200.gna as G
+    lib = G.load()
+    a = G.make_args(1, 1, 64, (64,), (16,), dtype=G.GNA_DTYPE_FP8_E4M3)
+    assert lib.gna_forward_ex(ctypes.byref(a)) == G.GNA_EUNSUPPORTED  # head_dim 64
+    a = G.make_args(1, 1, 128, (64,), (16,), dtype=G.GNA_DTYPE_FP8_E4M3, scales=(-1.0, 1.0, 1.0))
+    assert lib.gna_forward_ex(ctypes.byref(a)) == G.GNA_EINVAL
+    a = G.make_args(1, 1, 128, (64,), (16,), dtype=7)
+    assert lib.gna_forward_ex(ctypes.byref(a)) == G.GNA_EUNSUPPORTED

@@ -1,0 +1,68 @@
+"""GNA forward with E4M3 Q/K/V (GNA_DTYPE_FP8_E4M3)
+against the fp64 oracle run on the dequantised inputs.
+
+Tolerance (reading R17): the kernel's only rounding beyond the bf16 path is P -> E4M3
+before PV (RNE, 3 mantissa bits: relative error <= 2^-4 for P >= 2^-6, absolute <= 2^-10 below).
+With l >= 1 (the lazy running max never exceeds the row max), |dO| <= 2^-4 max|v| + n_small *
+2^-10 max|v| / l + bf16 output rounding; the rounding errors are unbiased, so their sum over the
+neighbourhood is far below the worst case.  Bound used: max-abs <= 2^-4 max|v| + 2e-2,
+mean-abs <= 2^-7 max|v| + 2e-3.  LSE depends only on fp32 row sums: 1e-3 as for bf16."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gna_inputs import make_qkv, quantize_e4m3
+
+@pytest.fixture(scope="module")
+def gna():
+    import paper_2504_16922_b200 as pkg
+    from paper_2504_16922_b200 import build
+
+    build.build()
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    pkg.load()
+    return pkg
+
+
+CFGS = [
+    dict(spatial=(256,), window=(32,), stride=(8,)),
+    dict(spatial=(40, 36), window=(9, 12), stride=(3, 4)),
+    dict(spatial=(37, 29), window=(8, 7), stride=(8, 7), dilation=(2, 2), causal=(False, True)),
+    dict(spatial=(12, 20, 18), window=(5, 8, 6), stride=(2, 3, 6), dilation=(1, 2, 1), causal=(True, False, False)),
+    dict(spatial=(64, 64), window=(32, 32), stride=(16, 16)),
+]
+
+
+def _ids(c):
+    return "x".join(map(str, c["spatial"])) + "_w" + "x".join(map(str, c["window"]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("disc", [False, True], ids=["normal", "discriminating"])
+@pytest.mark.parametrize("cfg", CFGS, ids=_ids)
+def test_fp8_forward_vs_oracle(gna, cfg, disc):
+    B, H, D = 2, 2, 128
+    q, k, v = make_qkv(B, cfg["spatial"], H, D, discriminating=disc, dtype=torch.float32)
+    (q8, qs, qd), (k8, ks, kd), (v8, vs, vd) = (quantize_e4m3(t) for t in (q, k, v))
+    out, lse = gna.forward(q8.cuda(), k8.cuda(), v8.cuda(), cfg["window"], cfg["stride"], cfg.get("dilation"),
+                           cfg.get("causal"), scales=(qs, ks, vs))
+    torch.cuda.synchronize()
+    assert out.dtype == torch.bfloat16
+    params = O.Params(cfg["spatial"], cfg["window"], cfg["stride"], cfg.get("dilation"), cfg.get("causal"))
+    ro, rl = O.forward(qd.numpy(), kd.numpy(), vd.numpy(), params)
+    o = out.float().cpu().numpy()
+    err = np.abs(o - ro)
+    vmax = float(vd.abs().max())
+    assert np.isfinite(o).all()
+    assert err.max() <= 2.0 ** -4 * vmax + 2e-2, f"O max-abs {err.max()}"
+    assert err.mean() <= 2.0 ** -7 * vmax + 2e-3, f"O mean-abs {err.mean()}"
+    assert np.abs(lse.cpu().numpy() - rl).max() <= 1e-3
+
+
+@pytest.mark.gpu
+def test_fp8_rejects_unsupported(gna):
+    q, k, v = make_qkv(1, (64,), 1, 64, dtype=torch.float32)
+    t8 = [quantize_e4m3(t)[0].cuda() for t in (q, k, v)]
+    with pytest.raises(gna.GnaError):
+        gna.forward(*t8, (16,), (4,))  # head_dim 64
