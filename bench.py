@@ -203,10 +203,18 @@ def run_ours(args, ws, rank, local):
     f = w.full()
     B, H, D = w.batch, w.heads, w.head_dim
     # weak scaling: rank r owns units [r*B*H, (r+1)*B*H) of a global batch N*B
-    qh, kh, vh = make_qkv(B, w.spatial, H, D, seed=SEED + 1000 * rank)
+    fp8 = args.dtype == "fp8"
+    scales = None
+    if fp8:  # E4M3 inputs with per-tensor scales, quantised on the host
+        from gna_inputs import quantize_e4m3
+        qf, kf, vf = make_qkv(B, w.spatial, H, D, seed=SEED + 1000 * rank, dtype=torch.float32)
+        (qh, qs, _), (kh, ks, _), (vh, vs, _) = (quantize_e4m3(t) for t in (qf, kf, vf))
+        scales = (qs, ks, vs)
+    else:
+        qh, kh, vh = make_qkv(B, w.spatial, H, D, seed=SEED + 1000 * rank)
     qh, kh, vh = (t.pin_memory() for t in (qh, kh, vh))
     q, k, v = (t.to(dev) for t in (qh, kh, vh))
-    out = torch.empty_like(q)
+    out = torch.empty(q.shape, dtype=torch.bfloat16, device=dev)
     lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=dev)
     info = gna.plan_info(B, H, D, **f)
     eff_flops = 4.0 * D * info["kept_pairs"] * B * H
@@ -215,7 +223,7 @@ def run_ours(args, ws, rank, local):
     win, st, dil, cau = f["window"], f["stride"], f["dilation"], f["causal"]
 
     def fwd():
-        gna.forward(q, k, v, win, st, dil, cau, out=out, lse=lse)
+        gna.forward(q, k, v, win, st, dil, cau, out=out, lse=lse, scales=scales)
 
     def timed(fn, steps):
         ts = []
@@ -255,14 +263,14 @@ def run_ours(args, ws, rank, local):
     # ---- per-stage times of the permuted pipeline (same stream, events between the
     #      three launches); warmed up first (workspace allocation is not timed)
     stage = {"permute": [], "attention": [], "unpermute": []}
-    o2 = torch.empty_like(q)
+    o2 = torch.empty_like(out)
     l2 = torch.empty_like(lse)
-    for _ in range(2):
+    for _ in range(0 if fp8 else 2):  # the E4M3 path has no stage API (permute-free only)
         gna.permute(q, k, v, o2, win, st, dil, cau)
         gna.attention_permuted(q, k, v, o2, win, st, dil, cau)
         gna.unpermute(q, k, v, o2, l2, win, st, dil, cau)
     torch.cuda.synchronize()
-    for _ in range(args.steps):
+    for _ in range(0 if fp8 else args.steps):
         flush.zero_()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record(stream)
@@ -279,14 +287,18 @@ def run_ours(args, ws, rank, local):
     # ---- dense baseline: same kernel, window = extent, same box (a6)
     dense_win = tuple(w.spatial)
     ones = tuple(1 for _ in w.spatial)
-    gna.forward(q, k, v, dense_win, ones, None, None, out=o2, lse=l2, box=info["box"])
-    gna.permute(q, k, v, o2, dense_win, ones, box=info["box"])
+    gna.forward(q, k, v, dense_win, ones, None, None, out=o2, lse=l2, box=info["box"], scales=scales)
+    if not fp8:
+        gna.permute(q, k, v, o2, dense_win, ones, box=info["box"])
     dense_ms = []
     for _ in range(max(3, min(args.steps, 10))):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        gna.attention_permuted(q, k, v, o2, dense_win, ones, box=info["box"])
+        if fp8:  # same kernel, window = extent (direct route)
+            gna.forward(q, k, v, dense_win, ones, None, None, out=o2, lse=l2, box=info["box"], scales=scales)
+        else:
+            gna.attention_permuted(q, k, v, o2, dense_win, ones, box=info["box"])
         e1.record(stream)
         e1.synchronize()
         dense_ms.append(e0.elapsed_time(e1))
@@ -308,7 +320,7 @@ def run_ours(args, ws, rank, local):
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
 
-    att_ms = statistics.mean(stage["attention"])
+    att_ms = statistics.mean(stage["attention"]) if not fp8 else statistics.mean(step_ms)
     # the default forward is permute-free (1 kernel) when the direct path applies
     direct = D >= 64 and all(b * d <= 256 and d <= 8 for b, d in zip(info["box"], list(f["dilation"]) + [1] * 3))
     launches_per_step = 1 if direct else 2
@@ -318,6 +330,8 @@ def run_ours(args, ws, rank, local):
         return
 
     peak_burst, peak_sus, hbm, peak_kind = _peaks()
+    if fp8:  # E4M3 dense peak = measured bf16 peak x the nominal ratio (4.5 / 2.25 PFLOP/s)
+        peak_burst, peak_sus, peak_kind = 2.0 * peak_burst, 2.0 * peak_sus, f"{peak_kind} bf16 x2 (nominal e4m3:bf16)"
     ms_per_step = total_ms / args.steps
     value = ws * eff_flops / (ms_per_step * 1e-3) / 1e12
     e2e_value = ws * eff_flops / (e2e_total / args.steps * 1e-3) / 1e12
@@ -328,6 +342,7 @@ def run_ours(args, ws, rank, local):
     mma_flops = 4.0 * info["padded_head_dim"] * 128 * 128 * info["subtile_stages"] * B * H  # issued (both GEMMs)
     n_tok = w.n_tokens
     nat_bytes = B * n_tok * H * D * 2
+    in_bytes = B * n_tok * H * D * (1 if fp8 else 2)  # one of q, k, v
     perm_bytes = 6 * nat_bytes  # read q,k,v + write permuted q,k,v (algorithmic, no padding)
     unperm_bytes = 2 * nat_bytes + 2 * B * n_tok * H * 4
     cpu = None
@@ -338,7 +353,7 @@ def run_ours(args, ws, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "vs_baseline": None, "dtype": "e4m3" if fp8 else "bf16", "data": "synthetic",
         "config": {"workload": w.name, "spatial": list(w.spatial), "window": list(w.window), "stride": list(w.stride),
                    "dilation": list(f["dilation"]), "causal": [int(c) for c in f["causal"]], "heads": H,
                    "head_dim": D, "batch_per_gpu": B, "global_batch": B * ws,
@@ -348,19 +363,19 @@ def run_ours(args, ws, rank, local):
         "bound": info["bound"],
         "speedup_frac_of_bound": (dense_max / att_ms_max) / info["bound"],
         "flopwise_speedup": float(n_tok * n_tok) / info["kept_pairs"] if not any(f["causal"]) else None,
-        "stages_ms": {k2: statistics.mean(v2) for k2, v2 in stage.items()},
+        "stages_ms": {k2: statistics.mean(v2) for k2, v2 in stage.items()} if not fp8 else None,
         "dense_attention_ms": statistics.mean(dense_ms),
         "dense_effective_tflops": 4.0 * D * n_tok * n_tok * B * H / (statistics.mean(dense_ms) * 1e-3) / 1e12,
-        "permute_gbs": perm_bytes / (statistics.mean(stage["permute"]) * 1e-3) / 1e9,
-        "unpermute_gbs": unperm_bytes / (statistics.mean(stage["unpermute"]) * 1e-3) / 1e9,
+        "permute_gbs": perm_bytes / (statistics.mean(stage["permute"]) * 1e-3) / 1e9 if not fp8 else None,
+        "unpermute_gbs": unperm_bytes / (statistics.mean(stage["unpermute"]) * 1e-3) / 1e9 if not fp8 else None,
         "mma_issued_tflops": mma_flops / (kernel_ms * 1e-3) / 1e12,
-        "permuted_pipeline_attention_tflops": eff_flops / (att_ms * 1e-3) / 1e12,
+        "permuted_pipeline_attention_tflops": eff_flops / (att_ms * 1e-3) / 1e12 if not fp8 else None,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s",
                      "frac": achieved / peak_burst, "traffic": _traffic_from_profiles(w.name),
                      "kernel": "gna_attn_sm100 (direct, one kernel per step)" if direct else "gna_attn_sm100",
-                     "peak_kind": f"{peak_kind} bf16 burst",
+                     "peak_kind": peak_kind if fp8 else f"{peak_kind} bf16 burst",
                      "frac_of_sustained": achieved / peak_sus},
-        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": 3 * nat_bytes,
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": 3 * in_bytes,
                 "d2h_bytes_per_step": nat_bytes + B * n_tok * H * 4},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
@@ -459,6 +474,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp8"],
+                    help="bf16 (default) or fp8: E4M3 Q/K/V with per-tensor scales (permute-free path)")
     ap.add_argument("--mode", default="weak", choices=["weak", "split"],
                     help="weak: each rank runs its own batch shard; split: Q-tile splitting of one problem")
     args = ap.parse_args()

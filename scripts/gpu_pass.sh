@@ -15,6 +15,11 @@ if [[ $WHAT == bench || $WHAT == all ]]; then
     timeout 600 python bench.py --workload $wl --steps 20 --warmup 5 > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err; echo "bench $wl rc=$?"; cut -c1-600 $OUT/bench_$wl.json
   done
 fi
+if [[ $WHAT == fp8 || $WHAT == all ]]; then
+  for wl in $WLS; do
+    timeout 600 python bench.py --workload $wl --dtype fp8 --steps 20 --warmup 5 --no-cpu-baseline > $OUT/bench_fp8_$wl.json 2> $OUT/bench_fp8_$wl.err; echo "bench fp8 $wl rc=$?"; cut -c1-300 $OUT/bench_fp8_$wl.json
+  done
+fi
 if [[ $WHAT == ncuattn ]]; then
   for wl in $WLS; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:gna_attn -s 3 -c 1 -o $OUT/attn_$wl \
