@@ -72,33 +72,20 @@ __global__ void __launch_bounds__(384, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
-    // ---------------------------------------------------------- work item
+    // ---------------------------------------------------------- work item: the load is issued
+    // first, its latency overlaps the barrier / TMEM set-up below
     const long long w = static_cast<long long>(blockIdx.x) + p.work_begin;
-    const long long bh = w / p.n_items;
-    const int4 item = p.items[w % p.n_items];
-    const int cls = item.x, subA = item.y, subB = item.z;
-    const bool hasB = subB >= 0;
-
-    int lo[3], hi[3];
-    sub_range(g, cls, subA, lo, hi);
-    if (hasB) {
-        int lb[3], hb[3];
-        sub_range(g, cls, subB, lb, hb);
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = min(lo[a], lb[a]);
-            hi[a] = max(hi[a], hb[a]);
-        }
+    long long bh, widx;
+    if ((w | p.n_items) < (1LL << 31)) {
+        const uint32_t w32 = static_cast<uint32_t>(w), n32 = static_cast<uint32_t>(p.n_items);
+        const uint32_t q32 = w32 / n32;
+        bh = q32;
+        widx = w32 - q32 * n32;
+    } else {
+        bh = w / p.n_items;
+        widx = w % p.n_items;
     }
-    int ext[3];
-    for (int a = 0; a < 3; ++a) ext[a] = hi[a] - lo[a];
-    const int nkv = ext[0] * ext[1] * ext[2];
-    const int nst_gna = (nkv + KPB - 1) / KPB;
-    if (nst_gna <= 0) return;  // uniform for the CTA: empty item
-    // extra (text) KV tokens: dense stages of 128 keys appended after the GNA stages
-    const int nst = nst_gna + p.extra_stages;
-
-    // rows of this (bh, class) start here in the permuted buffers
-    const long long cls_row0 = ((bh * g.ncls + cls) * static_cast<long long>(g.nbox)) * BV;
+    const int4 item = __ldg(p.items + widx);
 
     // ---------------------------------------------------------- smem carve
     const uint32_t sQ = sbase + C::Q_OFF;
@@ -144,6 +131,39 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+
+    const int cls = item.x, subA = item.y, subB = item.z;
+    const bool hasB = subB >= 0;
+
+    int lo[3], hi[3];
+    sub_range(g, cls, subA, lo, hi);
+    if (hasB) {
+        int lb[3], hb[3];
+        sub_range(g, cls, subB, lb, hb);
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = min(lo[a], lb[a]);
+            hi[a] = max(hi[a], hb[a]);
+        }
+    }
+    int ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = hi[a] - lo[a];
+    const int nkv = ext[0] * ext[1] * ext[2];
+    const int nst_gna = (nkv + KPB - 1) / KPB;
+    if (nst_gna <= 0) {  // uniform for the CTA: empty item (never planned; kept safe)
+        __syncthreads();
+        if (warp == 8) {
+            ptx::tc_fence_after();
+            ptx::tmem_dealloc(tmem, 512);
+        }
+        return;
+    }
+    // extra (text) KV tokens: dense stages of 128 keys appended after the GNA stages
+    const int nst = nst_gna + p.extra_stages;
+
+    // rows of this (bh, class) start here in the permuted buffers
+    const long long cls_row0 = ((bh * g.ncls + cls) * static_cast<long long>(g.nbox)) * BV;
+
+
 
     if (warp >= 8) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
