@@ -406,10 +406,33 @@ int plan_device_items(Plan& p, int4** out) {
         *out = it->second;
         return GNA_OK;
     }
+    // [items: n int4] then [info: 3 int4 per item] = {lo0, lo1, lo2, nkv}, {ext0, ext1, ext2, 0},
+    // {class coords c0, c1, c2, 0}: the union KV box range of the item's sub-tiles, decoded once on
+    // the host so the kernel's prologue has no integer divisions before its first TMA load
+    const size_t n = p.items.size();
+    std::vector<int4> buf(std::max<size_t>(1, 4 * n));
+    for (size_t i = 0; i < n; ++i) {
+        const int4 it = p.items[i];
+        int lo[3], hi[3];
+        sub_range(p.g, it.x, it.y, lo, hi);
+        if (it.z >= 0) {
+            int lb[3], hb[3];
+            sub_range(p.g, it.x, it.z, lb, hb);
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = std::min(lo[a], lb[a]);
+                hi[a] = std::max(hi[a], hb[a]);
+            }
+        }
+        int cc[3];
+        class_coords(p.g, it.x, cc);
+        buf[i] = it;
+        buf[n + 3 * i] = make_int4(lo[0], lo[1], lo[2], (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]));
+        buf[n + 3 * i + 1] = make_int4(hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 0);
+        buf[n + 3 * i + 2] = make_int4(cc[0], cc[1], cc[2], 0);
+    }
     int4* d = nullptr;
-    const size_t bytes = std::max<size_t>(1, p.items.size()) * sizeof(int4);
-    GNA_CUDA_TRY(cudaMalloc(&d, bytes));
-    if (!p.items.empty()) GNA_CUDA_TRY(cudaMemcpy(d, p.items.data(), p.items.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    GNA_CUDA_TRY(cudaMalloc(&d, buf.size() * sizeof(int4)));
+    GNA_CUDA_TRY(cudaMemcpy(d, buf.data(), buf.size() * sizeof(int4), cudaMemcpyHostToDevice));
     p.dev_items[dev] = d;
     *out = d;
     return GNA_OK;
@@ -628,6 +651,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.g = c.g;
     p.items = items;
     p.n_items = static_cast<long long>(c.plan->items.size());
+    p.item_info = items + p.n_items;
     const long long total = p.n_items * a->batch * a->heads;
     long long wb = a->work_begin, we = a->work_end;
     if (we <= 0 || we > total) we = total;

@@ -23,7 +23,7 @@ static __device__ unsigned long long g_gna_trace[GNA_TRACE_CTAS][GNA_TRACE_STAGE
     } while (0)
 // per-CTA timeline (all CTAs < GNA_TL_CTAS): globaltimer ns at events, plus the SM id
 #define GNA_TL_CTAS 8192
-static __device__ unsigned long long g_gna_tl[GNA_TL_CTAS][8];
+static __device__ unsigned long long g_gna_tl[GNA_TL_CTAS][16];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -86,6 +86,10 @@ __global__ void __launch_bounds__(384, 1)
         widx = w % p.n_items;
     }
     const int4 item = __ldg(p.items + widx);
+    const int4 inf_lo = __ldg(p.item_info + 3 * widx), inf_ext = __ldg(p.item_info + 3 * widx + 1),
+               inf_cc = __ldg(p.item_info + 3 * widx + 2);
+    const int b_idx32 = static_cast<int>(bh / static_cast<long long>(g.heads));  // bh < 2^31 x heads
+    const int h_idx32 = static_cast<int>(bh - static_cast<long long>(b_idx32) * g.heads);
 
     // ---------------------------------------------------------- smem carve
     const uint32_t sQ = sbase + C::Q_OFF;
@@ -131,23 +135,16 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_holder;
+    if (threadIdx.x == 0) GTL(8);
 
     const int cls = item.x, subA = item.y, subB = item.z;
     const bool hasB = subB >= 0;
 
-    int lo[3], hi[3];
-    sub_range(g, cls, subA, lo, hi);
-    if (hasB) {
-        int lb[3], hb[3];
-        sub_range(g, cls, subB, lb, hb);
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = min(lo[a], lb[a]);
-            hi[a] = max(hi[a], hb[a]);
-        }
-    }
-    int ext[3];
-    for (int a = 0; a < 3; ++a) ext[a] = hi[a] - lo[a];
-    const int nkv = ext[0] * ext[1] * ext[2];
+    // union KV box range of the item's sub-tiles (decoded on the host, plan_device_items)
+    const int lo[3] = {inf_lo.x, inf_lo.y, inf_lo.z};
+    const int ext[3] = {inf_ext.x, inf_ext.y, inf_ext.z};
+    const int ccl[3] = {inf_cc.x, inf_cc.y, inf_cc.z};  // dilation-class coordinates
+    const int nkv = inf_lo.w;
     const int nst_gna = (nkv + KPB - 1) / KPB;
     if (nst_gna <= 0) {  // uniform for the CTA: empty item (never planned; kept safe)
         __syncthreads();
@@ -162,8 +159,7 @@ __global__ void __launch_bounds__(384, 1)
 
     // rows of this (bh, class) start here in the permuted buffers
     const long long cls_row0 = ((bh * g.ncls + cls) * static_cast<long long>(g.nbox)) * BV;
-
-
+    if (threadIdx.x == 0) GTL(9);
 
     if (warp >= 8) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
@@ -182,10 +178,9 @@ __global__ void __launch_bounds__(384, 1)
             // NEXT-2): a 5-D box {64 cols, 1 head, B2, B1, B0 tokens} of the user's
             // heads-last tensor with element strides = dilation, so the TMA gathers the
             // class sub-grid itself and zero-fills past the tensor edges.
-            const long long b_idx = bh / g.heads;
-            const int h_idx = static_cast<int>(bh % g.heads);
-            int ccls[3];
-            class_coords(g, cls, ccls);
+            const long long b_idx = b_idx32;
+            const int h_idx = h_idx32;
+            const int* ccls = ccl;
             auto load_box = [&](const CUtensorMap* tm, uint32_t dst, uint32_t bar, int k0, int k1, int k2) {
                 if (p.direct) {
                     const int c2 = ccls[2] + g.ax[2].d * k2 * g.B[2];
@@ -212,6 +207,7 @@ __global__ void __launch_bounds__(384, 1)
                              sc[1] * g.QB[1] + u1, sc[2] * g.QB[2] + u2);
                 }
             }
+            GTL(10);
             int it = 0;
             StageBoxes sb;
             for (int j = 0; j < nst; ++j) {
@@ -281,6 +277,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
             };
             ptx::mbar_wait(bar_q, 0);
+            if (lane == 0) GTL(11);
             int it = 0;
             int slotK = it % C::NS;
             ptx::mbar_wait(bar_kv_full(slotK), (it / C::NS) & 1);
@@ -357,8 +354,8 @@ __global__ void __launch_bounds__(384, 1)
         const int sub = i == 0 ? subA : subB;
 
         // ---- this row's token and its per-axis window (class-local)
-        int cc[3], sc[3];
-        class_coords(g, cls, cc);
+        int sc[3];
+        const int cc[3] = {ccl[0], ccl[1], ccl[2]};
         sub_coords(g, sub, sc);
         const int ub = r / BV, inner = r % BV;
         const int u2 = ub % g.QB[2], u1 = (ub / g.QB[2]) % g.QB[1], u0 = ub / (g.QB[2] * g.QB[1]);
@@ -533,7 +530,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int a = 0; a < 3; ++a)
                 tok = tok * g.ax[a].L + (cc[a] + static_cast<long long>(g.ax[a].d) * (bx[a] * g.B[a] + xin[a]));
             const long long N = static_cast<long long>(g.ax[0].L) * g.ax[1].L * g.ax[2].L;
-            const long long b = bh / g.heads, h = bh % g.heads;
+            const long long b = b_idx32, h = h_idx32;
             const long long nat = (b * N + tok) * g.heads + h;
             orow = reinterpret_cast<__nv_bfloat16*>(p.out_nat) + nat * g.D;
             lrow = p.lse_nat != nullptr ? p.lse_nat + nat : nullptr;
@@ -568,8 +565,8 @@ __global__ void __launch_bounds__(384, 1)
             ptx::fence_proxy_async_smem();
             asm volatile("bar.sync %0, 128;" ::"r"(1 + i) : "memory");
             if (r == 0) {
-                const long long b_idx = bh / g.heads;
-                const int h_idx = static_cast<int>(bh % g.heads);
+                const long long b_idx = b_idx32;
+                const int h_idx = h_idx32;
 #pragma unroll
                 for (int u = 0; u < KPB; ++u) {
                     const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
@@ -698,7 +695,7 @@ extern "C" int gna_debug_timeline(void* host, size_t bytes) {
 }
 extern "C" int gna_debug_trace_reset(void) {
     static unsigned long long zeros[GNA_TRACE_CTAS * GNA_TRACE_STAGES * 16];
-    static unsigned long long zeros_tl[GNA_TL_CTAS * 8];
+    static unsigned long long zeros_tl[GNA_TL_CTAS * 16];
     if (cudaMemcpyToSymbol(g_gna_tl, zeros_tl, sizeof(zeros_tl)) != cudaSuccess) return 3;
     return cudaMemcpyToSymbol(g_gna_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 3;
 }

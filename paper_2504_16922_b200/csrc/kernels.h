@@ -12,6 +12,7 @@ namespace gna {
 struct AttnParams {
     Geometry g;
     const int4* items;      // work list: {class, subA, subB (-1 none), kv boxes}
+    const int4* item_info;  // per item 3 x int4: {lo[3], nkv}, {ext[3], 0}, {class coords[3], 0} (host-decoded)
     long long n_items;      // items per (batch, head)
     long long work_begin;   // global work range [work_begin, work_end) processed by the launch
     long long work_end;

@@ -29,7 +29,7 @@ for it in range(4):
     gna.forward(q, k, v, f["window"], f["stride"], f["dilation"], f["causal"],
                 flags=4 if os.environ.get("TRACE_PERMUTED") == "1" else 0)
     torch.cuda.synchronize()
-buf = np.zeros((8192, 8), dtype=np.uint64)
+buf = np.zeros((8192, 16) if not V4 else (8192, 8), dtype=np.uint64)
 assert lib.gna_debug_timeline(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
 if V4:
     # per task: 0 softmax setup start, 2 first S ready, 3 last P / stats, 4 epilogue done, 7 SM id
@@ -83,6 +83,14 @@ for i in range(n):
     busy[sm[i]] += rel[i, 5] - rel[i, 0]
 print(f"SMs used {len(np.unique(sm))}; mean SM busy {busy[busy>0].mean():.1f} us of span {span:.1f} "
       f"({busy[busy>0].mean()/span:.2f}); mainloop share of CTA time {d[:,2].sum()/d[:,5].sum():.2f}")
+if buf.shape[1] == 16:
+    e = buf[:n].astype(np.int64)
+    def med(a, b):
+        m = (e[:, a] > 0) & (e[:, b] > 0)
+        return np.median((e[m, b] - e[m, a]) / 1000.0) if m.any() else float("nan")
+    print("prologue (median us): start->syncthreads %.2f, ->decoded %.2f, producer decoded->Q issued %.2f, "
+          "Q issued->K issued %.2f, K issued->MMA Q ready %.2f, MMA Q ready->S0 ready %.2f" %
+          (med(0, 8), med(8, 9), med(9, 10), med(10, 1), med(1, 11), med(11, 2)))
 gaps = []
 for s_ in np.unique(sm):
     idx = np.where(sm == s_)[0]
