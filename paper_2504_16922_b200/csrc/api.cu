@@ -665,6 +665,16 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));
     p.scale_log2 = scale * 1.4426950408889634f;
     p.fp8 = fp8 ? 1 : 0;
+    {
+        static int sms = 0;
+        if (sms == 0) {
+            int dev = 0;
+            if (cudaGetDevice(&dev) != cudaSuccess ||
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+                sms = 148;
+        }
+        p.num_sms = sms;
+    }
     p.o_scale = 1.0f;
     if (fp8) {  // per-tensor dequantisation: S scales by q_scale*k_scale, O by v_scale
         p.scale_log2 *= (a->q_scale > 0.f ? a->q_scale : 1.f) * (a->k_scale > 0.f ? a->k_scale : 1.f);

@@ -37,6 +37,9 @@
 
 #include "attn_common.cuh"
 
+#ifndef GNA_NEXTWAVE_PF
+#define GNA_NEXTWAVE_PF 1  // L2 prefetch of the next wave's Q boxes (A/B: -DGNA_NEXTWAVE_PF=0)
+#endif
 #ifndef GNA_V3_ELECT
 #define GNA_V3_ELECT 1
 #endif
@@ -71,6 +74,17 @@ __global__ void __launch_bounds__(384, 1)
     const Geometry& g = p.g;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (warp == 8 && lane == 0) {
+        // descriptor fetches overlap the set-up below (the first TMA load otherwise waits for them)
+        ptx::tma_prefetch_desc(&tmap_q);
+        ptx::tma_prefetch_desc(&tmap_k);
+        ptx::tma_prefetch_desc(&tmap_v);
+        if (p.n_extra > 0) {
+            ptx::tma_prefetch_desc(&tmap_ek);
+            ptx::tma_prefetch_desc(&tmap_ev);
+        }
+        if (p.tma_store) ptx::tma_prefetch_desc(&p.tmap_o);
+    }
 
     // ---------------------------------------------------------- work item: the load is issued
     // first, its latency overlaps the barrier / TMEM set-up below
@@ -166,13 +180,6 @@ __global__ void __launch_bounds__(384, 1)
       if (warp == 8) {
         // ===================================================== TMA producer
         if (lane == 0) {
-            ptx::tma_prefetch_desc(&tmap_q);
-            ptx::tma_prefetch_desc(&tmap_k);
-            ptx::tma_prefetch_desc(&tmap_v);
-            if (p.n_extra > 0) {
-                ptx::tma_prefetch_desc(&tmap_ek);
-                ptx::tma_prefetch_desc(&tmap_ev);
-            }
             // One box of 64/128 token rows, both D halves.  Permuted mode: a contiguous row
             // range of the permuted tensor (2-D map).  Direct mode (permute-free, SURVEY
             // NEXT-2): a 5-D box {64 cols, 1 head, B2, B1, B0 tokens} of the user's
@@ -232,6 +239,34 @@ __global__ void __launch_bounds__(384, 1)
                         for (int h = 0; h < C::NH; ++h)
                             ptx::tma_load_3d(sKV + slot * C::TILE_BYTES + h * C::CHUNK_BYTES, tm, bar_kv_full(slot), h * 64,
                                              h_idx, row);
+                    }
+                }
+            }
+            // All loads issued: warm L2 with the Q boxes of the CTA that will most likely follow on this
+            // SM (one wave later, blockIdx + #SMs), so its first QK^T does not wait on HBM latency.
+            const long long w2 = w + p.num_sms;
+            if (GNA_NEXTWAVE_PF && p.num_sms > 0 && w2 < p.work_end) {
+                const long long bh2 = w2 / p.n_items, widx2 = w2 - bh2 * p.n_items;
+                const int4 it2 = __ldg(p.items + widx2);
+                const int4 cc2 = __ldg(p.item_info + 3 * widx2 + 2);
+                const int b2 = static_cast<int>(bh2 / g.heads), h2 = static_cast<int>(bh2 % g.heads);
+                const long long row0_2 = ((bh2 * g.ncls + it2.x) * static_cast<long long>(g.nbox)) * BV;
+                for (int i = 0; i < (it2.z >= 0 ? 2 : 1); ++i) {
+                    int sc2[3];
+                    sub_coords(g, i == 0 ? it2.y : it2.z, sc2);
+                    for (int u = 0; u < KPB; ++u) {
+                        const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
+                        const int k0 = sc2[0] * g.QB[0] + u0, k1 = sc2[1] * g.QB[1] + u1, k2 = sc2[2] * g.QB[2] + u2;
+#pragma unroll
+                        for (int h = 0; h < C::NH; ++h) {
+                            if (p.direct)
+                                ptx::tma_prefetch_5d(&tmap_q, h * 64, h2, cc2.z + g.ax[2].d * k2 * g.B[2],
+                                                     cc2.y + g.ax[1].d * k1 * g.B[1],
+                                                     b2 * g.ax[0].L + cc2.x + g.ax[0].d * k0 * g.B[0]);
+                            else
+                                ptx::tma_prefetch_2d(&tmap_q, h * 64,
+                                                     static_cast<int>(row0_2 + static_cast<long long>((k0 * g.nb[1] + k1) * g.nb[2] + k2) * BV));
+                        }
                     }
                 }
             }

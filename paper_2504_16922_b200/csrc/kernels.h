@@ -29,6 +29,7 @@ struct AttnParams {
     // O written by TMA stores from smem (v3): 0 = per-thread stores, 1 = 2-D map over the
     // permuted O rows, 2 = 5-D map over the user's O [B][s0][s1][s2][H][D] (clips padding)
     int tma_store;
+    int num_sms;            // v3: the SM count (L2 prefetch of the next wave's Q boxes: CTA + num_sms)
     int fp8;                // 1: Q/K/V are E4M3, per-tensor scales folded in below
     float o_scale;          // O multiplier (v_scale for FP8, 1 for bf16)
     CUtensorMap tmap_o;
