@@ -66,3 +66,29 @@ def test_fp8_rejects_unsupported(gna):
     t8 = [quantize_e4m3(t)[0].cuda() for t in (q, k, v)]
     with pytest.raises(gna.GnaError):
         gna.forward(*t8, (16,), (4,))  # head_dim 64
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c2b_flux64_s16", "c4a_hunyuan_blocked", "c3_cosmos"])
+def test_fp8_full_size_sampled(gna, name):
+    """E4M3 forward at BASELINE.json's full sizes (the launch bench.py --dtype fp8 times), sampled
+    rows incl. grid corners vs the oracle on the dequantised inputs; same tolerance as above."""
+    from gna_inputs import WORKLOADS, sample_rows
+    w = WORKLOADS[name]
+    f = w.full()
+    q, k, v = make_qkv(w.batch, w.spatial, w.heads, w.head_dim, dtype=torch.float32)
+    (q8, qs, qd), (k8, ks, kd), (v8, vs, vd) = (quantize_e4m3(t) for t in (q, k, v))
+    out, lse = gna.forward(q8.cuda(), k8.cuda(), v8.cuda(), f["window"], f["stride"], f["dilation"], f["causal"],
+                           scales=(qs, ks, vs))
+    torch.cuda.synchronize()
+    L = list(w.spatial) + [1] * (3 - len(w.spatial))
+    corners = [0, L[1] * L[2] - 1, w.n_tokens - 1, (L[0] // 2) * L[1] * L[2] + (L[1] // 2) * L[2] + L[2] // 2]
+    rows = sample_rows(w.batch, w.spatial, w.heads, 64, extra_tokens=corners)
+    ro, rl, _ = O.forward_rows(qd.numpy(), kd.numpy(), vd.numpy(), O.Params(**f), rows)
+    oo = out.float().cpu().reshape(w.batch, -1, w.heads, w.head_dim)[rows[:, 0], rows[:, 1], rows[:, 2]].numpy()
+    ll = lse.cpu().reshape(w.batch, -1, w.heads)[rows[:, 0], rows[:, 1], rows[:, 2]].numpy()
+    err = np.abs(oo - ro)
+    vmax = float(vd.abs().max())
+    assert err.max() <= 2.0 ** -4 * vmax + 2e-2, f"O max-abs {err.max()}"
+    assert err.mean() <= 2.0 ** -7 * vmax + 2e-3, f"O mean-abs {err.mean()}"
+    assert np.abs(ll - rl).max() <= 1e-3
