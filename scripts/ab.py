@@ -33,12 +33,13 @@ def run(workloads, names):
                 for kv in filter(None, envspec.split(",")):
                     k, _, v = kv.partition("=")
                     env[k] = v
+                extra = os.environ.get("AB_ARGS", "").split()
                 out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", wl, "--steps", "10",
-                                      "--warmup", "3", "--no-cpu-baseline"], env=env, capture_output=True, text=True,
-                                     timeout=600)
+                                      "--warmup", "3", "--no-cpu-baseline", *extra], env=env, capture_output=True,
+                                     text=True, timeout=600)
                 try:
                     d = json.loads(out.stdout.strip().splitlines()[-1])
-                    res.setdefault((name, wl), []).append((d["value"], d["permuted_pipeline_attention_tflops"],
+                    res.setdefault((name, wl), []).append((d["value"], d.get("permuted_pipeline_attention_tflops") or 0.0,
                                                            d["clocks"]["sm_mhz"]))
                 except Exception:
                     res.setdefault((name, wl), []).append(("ERR", out.stderr[-300:]))
