@@ -40,6 +40,9 @@
 #ifndef GNA_NEXTWAVE_PF
 #define GNA_NEXTWAVE_PF 1  // L2 prefetch of the next wave's Q boxes (A/B: -DGNA_NEXTWAVE_PF=0)
 #endif
+#ifndef GNA_SPEC_EXP
+#define GNA_SPEC_EXP 0  // speculative exponentials of P chunk 0 with the running max: measured 20% slower (spills), A/B only
+#endif
 #ifndef GNA_V3_ELECT
 #define GNA_V3_ELECT 1
 #endif
@@ -467,15 +470,77 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int c = 0; c < 128; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
             }
-            float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
+            // Exponentials of P chunk 0 are computed speculatively with the current running max
+            // while the tile max is reduced (the MUFU and the FMNMX3 ALU work interleave); they are
+            // redone -- rarely: only when some row's max grows by > 8 (log2 units) -- with the
+            // raised max.  The results are bit-identical to computing the max first.
+            constexpr int CH = 64 / GNA_PSPLIT;  // key pairs per P chunk
+            float la0 = 0.f, la1 = 0.f, lb0 = 0.f, lb1 = 0.f;
+            uint32_t pk[64];
+            auto do_pair = [&](int pi, float neg) {
+                // x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU or, for 1 pair in GNA_POLY_EVERY, on the
+                // FMA pipe (polynomial); row sum with FADD2; pack to bf16x2 (or E4M3, 4 keys per column)
+                float x0, x1, y0, y1;
+                ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
+                if (GNA_POLY_EVERY > 0 && (pi % (GNA_POLY_EVERY > 0 ? GNA_POLY_EVERY : 1)) == GNA_POLY_EVERY - 1) {
+                    ptx::ex2_poly2(y0, y1, x0, x1);
+                } else {
+                    y0 = ptx::ex2(x0);
+                    y1 = ptx::ex2(x1);
+                }
+                if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
+                else ptx::fadd2(la0, la1, la0, la1, y0, y1);
+                if constexpr (F8) {
+                    const uint32_t h16 = ptx::pack_e4m3x2(y0, y1);  // P <= 2^8 by the lazy max: in range
+                    if (pi & 1) pk[pi >> 1] |= h16 << 16;
+                    else pk[pi >> 1] = h16;
+                } else {
+                    pk[pi] = ptx::pack_bf16x2(y0, y1);
+                }
+            };
+            auto tile_max = [&]() {
+                float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
 #pragma unroll
-            for (int c = 4; c < 128; c += 8) {
-                mx0 = ptx::max3(mx0, s[c], s[c + 1]);
-                mx1 = ptx::max3(mx1, s[c + 2], s[c + 3]);
-                mx2 = ptx::max3(mx2, s[c + 4], s[c + 5]);
-                mx3 = ptx::max3(mx3, s[c + 6], s[c + 7]);
+                for (int c = 4; c < 128; c += 8) {
+                    mx0 = ptx::max3(mx0, s[c], s[c + 1]);
+                    mx1 = ptx::max3(mx1, s[c + 2], s[c + 3]);
+                    mx2 = ptx::max3(mx2, s[c + 4], s[c + 5]);
+                    mx3 = ptx::max3(mx3, s[c + 6], s[c + 7]);
+                }
+                return ptx::max3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
+            };
+            // store the P columns of the chunk ending at pair pi (keys [2*(pi+1-CH), 2*(pi+1))) and,
+            // except for the last chunk, let the MMA start the PV on them right away
+            auto store_chunk = [&](int pi) {
+                const int c0 = pi + 1 - CH;
+                if constexpr (F8) {
+                    if (CH == 64) ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
+                    else ptx::tmem_st16(tS + c0 / 2, &pk[c0 / 2]);
+                } else if (CH == 32) ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
+                else if (CH == 16) ptx::tmem_st16(tS + c0, &pk[c0]);
+                else {
+                    ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
+                    ptx::tmem_st32(tS + c0 + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0 + 32]));
+                }
+                if (pi < 63) {
+                    ptx::tmem_wait_st();
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(bar_pc0 + 8 * (3 * i + pi / CH));
+                }
+            };
+            const bool spec = GNA_SPEC_EXP && j > 0 && __all_sync(0xffffffffu, m_used != -INFINITY);
+            float m_tile;
+            bool redo = true;
+            if (spec) {
+                const float neg0 = -m_used;
+#pragma unroll
+                for (int pi = 0; pi < CH; ++pi) do_pair(pi, neg0);
+                m_tile = tile_max();
+                redo = __any_sync(0xffffffffu, m_tile > m_used + 8.0f);
+                if (redo) la0 = la1 = lb0 = lb1 = 0.f;
+            } else {
+                m_tile = tile_max();
             }
-            const float m_tile = ptx::max3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
             const float m_new = fmaxf(m_used, m_tile);
             if (r == 0) GT(j, 4 * i + 2);
             const bool need = m_new > m_used + 8.0f;
@@ -496,50 +561,15 @@ __global__ void __launch_bounds__(384, 1)
                 m_used = m_new;
             }
             const float neg = m_used == -INFINITY ? 0.f : -m_used;
-            // x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU for 3 of every 4 pairs and
-            // on the FMA pipe (polynomial) for the 4th, row sum with FADD2, pack to bf16x2.
-            float la0 = 0.f, la1 = 0.f, lb0 = 0.f, lb1 = 0.f;
-            uint32_t pk[64];
+            if (redo) {
 #pragma unroll
-            for (int pi = 0; pi < 64; ++pi) {
-                float x0, x1, y0, y1;
-                ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
-                if (GNA_POLY_EVERY > 0 && (pi % (GNA_POLY_EVERY > 0 ? GNA_POLY_EVERY : 1)) == GNA_POLY_EVERY - 1) {
-                    ptx::ex2_poly2(y0, y1, x0, x1);
-                } else {
-                    y0 = ptx::ex2(x0);
-                    y1 = ptx::ex2(x1);
-                }
-                if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
-                else ptx::fadd2(la0, la1, la0, la1, y0, y1);
-                constexpr int CH = 64 / GNA_PSPLIT;  // key pairs per P chunk
-                if constexpr (F8) {
-                    // E4M3 P (P <= 2^8 by the lazy max, inside E4M3's range): 4 keys per TMEM column
-                    const uint32_t h16 = ptx::pack_e4m3x2(y0, y1);
-                    if (pi & 1) pk[pi >> 1] |= h16 << 16;
-                    else pk[pi >> 1] = h16;
-                } else {
-                    pk[pi] = ptx::pack_bf16x2(y0, y1);
-                }
-                if (pi % CH == CH - 1) {
-                    // P columns of this chunk (keys [2*(pi+1-CH), 2*(pi+1))) are final: store them and,
-                    // except for the last chunk, let the MMA start the PV on them right away
-                    const int c0 = pi + 1 - CH;
-                    if constexpr (F8) {
-                        if (CH == 64) ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
-                        else ptx::tmem_st16(tS + c0 / 2, &pk[c0 / 2]);
-                    } else if (CH == 32) ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
-                    else if (CH == 16) ptx::tmem_st16(tS + c0, &pk[c0]);
-                    else {
-                        ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
-                        ptx::tmem_st32(tS + c0 + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0 + 32]));
-                    }
-                    if (pi < 63) {
-                        ptx::tmem_wait_st();
-                        ptx::tc_fence_before();
-                        ptx::mbar_arrive(bar_pc0 + 8 * (3 * i + pi / CH));
-                    }
-                }
+                for (int pi = 0; pi < CH; ++pi) do_pair(pi, neg);
+            }
+            store_chunk(CH - 1);
+#pragma unroll
+            for (int pi = CH; pi < 64; ++pi) {
+                do_pair(pi, neg);
+                if (pi % CH == CH - 1) store_chunk(pi);
             }
             l_run += (la0 + la1) + (lb0 + lb1);
             ptx::tmem_wait_st();
