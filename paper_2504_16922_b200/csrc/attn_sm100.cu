@@ -40,6 +40,12 @@
 #ifndef GNA_NEXTWAVE_PF
 #define GNA_NEXTWAVE_PF 1  // L2 prefetch of the next wave's Q boxes (A/B: -DGNA_NEXTWAVE_PF=0)
 #endif
+// register split (setmaxnreg): the launch reserves 168 x 384 = 64512 registers; softmax warpgroups x 2
+// + control warpgroup must fit: 2 x 128 x SM + 128 x CTRL <= 64512
+#ifndef GNA_V3_SM_REGS
+#define GNA_V3_SM_REGS "216"
+#define GNA_V3_CTRL_REGS "64"
+#endif
 #ifndef GNA_SPEC_EXP
 #define GNA_SPEC_EXP 0  // speculative exponentials of P chunk 0 with the running max: measured 20% slower (spills), A/B only
 #endif
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(384, 1)
     if (threadIdx.x == 0) GTL(9);
 
     if (warp >= 8) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 " GNA_V3_CTRL_REGS ";\n" ::: "memory");
       if (warp == 8) {
         // ===================================================== TMA producer
         if (lane == 0) {
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
     } else {
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 " GNA_V3_SM_REGS ";\n" ::: "memory");
       if (warp < 4 || hasB) {
         // ==================================================== softmax WG i
         const int i = warp >> 2;
