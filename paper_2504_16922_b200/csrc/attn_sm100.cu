@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(384, 1)
       if (warp == 8) {
         // ===================================================== TMA producer
         if (lane == 0) {
+            GTL(12);
             // One box of 64/128 token rows, both D halves.  Permuted mode: a contiguous row
             // range of the permuted tensor (2-D map).  Direct mode (permute-free, SURVEY
             // NEXT-2): a 5-D box {64 cols, 1 head, B2, B1, B0 tokens} of the user's
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
             };
             ptx::mbar_expect_tx(bar_q, (hasB ? 2 : 1) * C::TILE_BYTES);
+            GTL(13);
             for (int i = 0; i < (hasB ? 2 : 1); ++i) {
                 const int sub = i == 0 ? subA : subB;
                 int sc[3];
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(384, 1)
                     const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
                     load_box(&tmap_q, sQ + i * C::TILE_BYTES + u * BV * 128, bar_q, sc[0] * g.QB[0] + u0,
                              sc[1] * g.QB[1] + u1, sc[2] * g.QB[2] + u2);
+                    if (i == 0 && u == 0) GTL(14);
                 }
             }
             GTL(10);

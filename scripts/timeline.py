@@ -88,6 +88,8 @@ if buf.shape[1] == 16:
     def med(a, b):
         m = (e[:, a] > 0) & (e[:, b] > 0)
         return np.median((e[m, b] - e[m, a]) / 1000.0) if m.any() else float("nan")
+    print("producer (median us): decoded->producer start %.2f, ->expect_tx %.2f, ->first Q TMA issued %.2f, "
+          "->all Q issued %.2f" % (med(9, 12), med(12, 13), med(13, 14), med(14, 10)))
     print("prologue (median us): start->syncthreads %.2f, ->decoded %.2f, producer decoded->Q issued %.2f, "
           "Q issued->K issued %.2f, K issued->MMA Q ready %.2f, MMA Q ready->S0 ready %.2f" %
           (med(0, 8), med(8, 9), med(9, 10), med(10, 1), med(1, 11), med(11, 2)))
