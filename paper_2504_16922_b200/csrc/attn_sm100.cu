@@ -8,7 +8,7 @@
 // Warp roles (384 threads, registers re-balanced with setmaxnreg):
 //   warps 0-3  softmax WG0 : rows of sub-tile A, TMEM lanes 0-127, S0/P0, O0 (224 regs)
 //   warps 4-7  softmax WG1 : rows of sub-tile B, S1/P1, O1                   (224 regs)
-//   warp  8    TMA producer: Q sub-tiles once, then K_j, V_j into a smem ring (56 regs)
+//   warp  8    TMA producer: K_j, V_j into a smem ring; warp 10: the Q sub-tiles (64 regs)
 //   warp  9    MMA issuer  : tcgen05.mma, one elected lane
 //   warps 10-11 idle (complete the control warpgroup for setmaxnreg)
 // TMEM (512 columns x 128 lanes, fp32):  S0 [0,128)  S1 [128,256)
@@ -45,6 +45,9 @@
 #ifndef GNA_V3_SM_REGS
 #define GNA_V3_SM_REGS "216"
 #define GNA_V3_CTRL_REGS "64"
+#endif
+#ifndef GNA_Q_WARP10
+#define GNA_Q_WARP10 1  // warp 10 issues the Q loads while warp 8 starts the K/V stream (0: one producer, A/B)
 #endif
 #ifndef GNA_SPEC_EXP
 #define GNA_SPEC_EXP 0  // speculative exponentials of P chunk 0 with the running max: measured 20% slower (spills), A/B only
@@ -186,8 +189,9 @@ __global__ void __launch_bounds__(384, 1)
 
     if (warp >= 8) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 " GNA_V3_CTRL_REGS ";\n" ::: "memory");
-      if (warp == 8) {
-        // ===================================================== TMA producer
+      if (warp == 8 || (GNA_Q_WARP10 && warp == 10)) {
+        // ===================================================== TMA producer (warp 8: K/V; the Q
+        // sub-tiles from warp 10 when GNA_Q_WARP10, so the two streams issue in parallel)
         if (lane == 0) {
             GTL(12);
             // One box of 64/128 token rows, both D halves.  Permuted mode: a contiguous row
@@ -212,6 +216,7 @@ __global__ void __launch_bounds__(384, 1)
                     for (int h = 0; h < C::NH; ++h) ptx::tma_load_2d(dst + h * C::CHUNK_BYTES, tm, bar, h * 64, row);
                 }
             };
+            if (!GNA_Q_WARP10 || warp == 10) {
             ptx::mbar_expect_tx(bar_q, (hasB ? 2 : 1) * C::TILE_BYTES);
             GTL(13);
             for (int i = 0; i < (hasB ? 2 : 1); ++i) {
@@ -227,6 +232,8 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             GTL(10);
+            }
+            if (warp == 8) {
             int it = 0;
             StageBoxes sb;
             for (int j = 0; j < nst; ++j) {
@@ -282,6 +289,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             }
+            }  // warp == 8
         }
     } else if (warp == 9) {
         // ======================================================= MMA issuer

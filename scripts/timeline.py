@@ -8,7 +8,7 @@ import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2504_16922_b200 import build
 import paper_2504_16922_b200.gna as G
-G.LIB_PATH = build.build(trace=True)
+G.LIB_PATH = os.environ.get("TRACE_LIB") or build.build(trace=True)
 import numpy as np, torch
 import paper_2504_16922_b200 as gna
 from gna_inputs import WORKLOADS, make_qkv
