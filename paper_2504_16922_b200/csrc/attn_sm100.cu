@@ -6,11 +6,12 @@
 // ever exists in HBM, and boxes outside the range are never loaded.
 //
 // Warp roles (384 threads, registers re-balanced with setmaxnreg):
-//   warps 0-3  softmax WG0 : rows of sub-tile A, TMEM lanes 0-127, S0/P0, O0 (224 regs)
-//   warps 4-7  softmax WG1 : rows of sub-tile B, S1/P1, O1                   (224 regs)
-//   warp  8    TMA producer: K_j, V_j into a smem ring; warp 10: the Q sub-tiles (64 regs)
+//   warps 0-3  softmax WG0 : rows of sub-tile A, TMEM lanes 0-127, S0/P0, O0 (216 regs)
+//   warps 4-7  softmax WG1 : rows of sub-tile B, S1/P1, O1                   (216 regs)
+//   warp  8    TMA producer: K_j, V_j into a smem ring                     (64 regs)
 //   warp  9    MMA issuer  : tcgen05.mma, one elected lane
-//   warps 10-11 idle (complete the control warpgroup for setmaxnreg)
+//   warp  10   TMA producer: the Q sub-tiles (in parallel with warp 8)
+//   warp  11   idle (completes the control warpgroup for setmaxnreg)
 // TMEM (512 columns x 128 lanes, fp32):  S0 [0,128)  S1 [128,256)
 //   O0 [256, 256+Dp)  O1 [384, 384+Dp); P_i (bf16x2) aliases S_i's first 64.
 //
