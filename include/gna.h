@@ -18,6 +18,7 @@
  *
  * Layout (a build decision -- the paper states none; heads-last as NATTEN):
  *   q, k, v, out : bf16 [batch][s0][s1][s2][heads][head_dim], contiguous
+ *                  (GNA_DTYPE_FP8_E4M3: q, k, v are E4M3 bytes, same shape; out stays bf16)
  *   lse          : fp32 [batch][s0][s1][s2][heads]
  *   1-D problems pass spatial = {L, 1, 1}; unused axes must be exactly
  *   window = stride = dilation = 1, causal = 0.
