@@ -59,11 +59,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 #define GNA_PROG(slot, val) \
     do {                    \
     } while (0)
+#ifndef GNA_WAIT_HINT
+#define GNA_WAIT_HINT 0  // 1: try_wait with a suspend-time hint (A/B)
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
+#if GNA_WAIT_HINT
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+#endif
         "@!p bra WAIT_%=;\n}" ::"r"(bar),
         "r"(parity)
         : "memory");
