@@ -13,7 +13,12 @@
  *     of its leader, the center-most member, right-biased;
  *   - the leader's window has floor(w/2) keys on the left and is
  *     shifted inward at borders so every query sees w keys;
- *   - causal axes (cited only) use DESIGN.md reading R4.
+ *   - causal axes (cited only) use DESIGN.md reading R4: the group
+ *     leader is the LAST member of its stride group and the keys are
+ *     [max(0, leader - w + 1), i] (s = 1: causal sliding window; s = w: block
+ *     causal; every query attends itself).  NOTE: this differs from SPEC's
+ *     reading (center leader, then intersect with [0, i]) for stride >= 3; the
+ *     two coincide for stride <= 2.
  *   out[q] = softmax_k(scale * q.k) v,   lse[q] = ln sum_k exp(scale * q.k).
  *
  * Layout (a build decision -- the paper states none; heads-last as NATTEN):
@@ -51,10 +56,18 @@
  *     aligned; the library never frees them.  Work is enqueued on the given
  *     stream (NULL = legacy default stream); no host synchronisation except in
  *     the gna_debug_* exports, which copy small arrays to host memory.
- *   - Workspace: the permuted Q/K/V/O/LSE buffers and the work list come from
- *     the caller's workspace (gna_args.workspace, sized by
- *     gna_workspace_size) or, when NULL, from a per-device grow-only cache
- *     owned by the library (mutex-guarded), freed by gna_release_workspace().
+ *   - Workspace (permuted route only): the permuted Q/K/V/O/LSE buffers come
+ *     from the caller's workspace (gna_args.workspace, sized by
+ *     gna_workspace_size) or, when NULL, from a library cache keyed by
+ *     (device, stream), grown stream-ordered (cudaMallocAsync) and never
+ *     freed before gna_release_workspace() (outgrown buffers are retired, so
+ *     queued work and captured graphs stay valid).  Growth inside a CUDA graph
+ *     capture is refused (GNA_EINVAL): for graphs, pass a workspace or call
+ *     once before capturing.
+ *   - Work lists: planned on the host once per parameter tuple (cached until
+ *     gna_release_workspace) and uploaded per device with an async copy on
+ *     the first launching stream (other streams wait on its event).  The
+ *     first call for a problem must not be inside a graph capture.
  *   - There is no CPU fallback: a missing sm_100 device is GNA_EUNSUPPORTED.
  *   - Validation: 1 <= stride <= window, window*dilation <=
  *     extent, all values >= 1, causal in {0,1}, batch, heads >= 1,
@@ -93,6 +106,9 @@ extern "C" {
                                         writes O and LSE straight into the user layout) */
 #define GNA_FLAG_PERMUTED 4          /* gna_forward_ex: use the permute -> attention path even when
                                         the permute-free (direct 5-D TMA) path is available */
+#define GNA_FLAG_WORK_RANGE 8        /* take [work_begin, work_end) literally (begin == end is an
+                                        empty launch); without it, end <= 0 means "to the end" and
+                                        {0, 0} (a zero-initialised struct) means all work items */
 
 typedef struct gna_args {
     const void *q, *k, *v; /* device bf16 [B][s0][s1][s2][H][D] */
@@ -107,8 +123,11 @@ typedef struct gna_args {
     size_t workspace_bytes;
     int box[3];             /* permutation box / KV tile override (powers of two,
                                volume 64 or 128); {0,0,0} = planner's choice */
-    long long work_begin;   /* Q-tile splitting: global work-item range [begin, end) */
-    long long work_end;     /* over (batch*heads) x items; end <= 0 -> all   */
+    long long work_begin;   /* Q-tile splitting: global work-item range [begin, end) over   */
+    long long work_end;     /* the n_work = batch*heads*n_items items, unit-major (item w of
+                               the launch = unit w / n_items, u = b*heads + h).  Without
+                               GNA_FLAG_WORK_RANGE, end <= 0 -> to the end.  Outside
+                               [0, n_work] or begin > end: GNA_EINVAL. */
     int flags;
     /* Extra (text) KV tokens fused into the same kernel:
      * n_extra keys/values per (batch, head), layout bf16 [B][n_extra][H][D],
@@ -188,8 +207,12 @@ int gna_sim_sweep(const gna_sim_args *a, int32_t *strides_out, gna_sim_report *r
  * `steps` diffusion steps kept dense, the rest sped up by op_speedup. */
 double gna_sim_e2e(double sa_share, int steps, int sa_steps, double op_speedup);
 
-/* Full forward: permute -> attention -> inverse permute, on the legacy default
- * stream with the library workspace.  Arguments as in gna_args. */
+/* Full forward (the north-star entry point), bf16, on the legacy default stream.
+ * Same route as gna_forward_ex with default options: for head_dim >= 64 and
+ * box*dilation <= 256 per axis, ONE kernel (5-D TMA gathers from q/k/v, O and
+ * LSE scattered by the epilogue); otherwise permute -> attention with the
+ * inverse permutation fused into the epilogue, using the library workspace.
+ * Arguments as in gna_args; lse may be NULL. */
 int gna_forward(const void *q, const void *k, const void *v, void *out, float *lse,
                 int batch, int heads, int head_dim, const int spatial[3], const int window[3],
                 const int stride[3], const int dilation[3], const int causal[3], float scale);
@@ -220,7 +243,8 @@ int gna_debug_visits(const gna_args *a, int32_t *host_out, long long *n_records)
 /* work list: int32 [n_items][4] = {class, subA, subB (-1 = none), kv_boxes} */
 int gna_debug_worklist(const gna_args *a, int32_t *host_out, long long *n_items);
 
-/* Free the library-owned workspace cache of the current device. */
+/* Synchronise the current device, then free the library-owned workspaces
+ * (every stream) and the device work lists of the current device. */
 int gna_release_workspace(void);
 
 /* Thread-local message for the last non-OK return. */

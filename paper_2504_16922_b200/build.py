@@ -7,8 +7,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "attn_sm100.cu", "attn_v4.cu", "permute.cu", "sim.cpp"]
-HEADERS = ["geom.cuh", "ptx.cuh", "kernels.h", "attn_persistent.cuh", "attn_common.cuh", os.path.join("..", "..", "include", "gna.h")]
+SOURCES = ["api.cu", "attn_sm100.cu", "permute.cu", "sim.cpp"]
+HEADERS = ["geom.cuh", "ptx.cuh", "kernels.h", "attn_common.cuh", os.path.join("..", "..", "include", "gna.h")]
 OUT = os.path.join(HERE, "libgna_b200.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]

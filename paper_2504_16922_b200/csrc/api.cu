@@ -129,11 +129,22 @@ int validate(const gna_args* a, bool need_ptrs) {
 }
 
 // ------------------------------------------------------------------- plans
+// Per-device copy of a plan's work list: uploaded once with an async copy on the first
+// launching stream; later launches on other streams wait for it through `ready` (a device-side
+// event wait, no host synchronisation).
+struct DevItems {
+    int4* ptr = nullptr;
+    cudaEvent_t ready = nullptr;
+    bool done = false;  // the upload is known complete (no wait needed)
+};
+
 struct Plan {
     Geometry g;  // batch/heads filled per call
     std::vector<int4> items;
     gna_plan_info_t info;
-    std::map<int, int4*> dev_items;  // per device copy of the work list
+    int4* host_items = nullptr;  // pinned [items | 3 x info per item], source of the async uploads
+    size_t host_count = 0;
+    std::map<int, DevItems> dev_items;
     std::mutex mu;
 };
 
@@ -360,57 +371,17 @@ std::shared_ptr<Plan> get_plan(const gna_args* a) {
     return plan;
 }
 
-// Persistent-kernel work queue counters: a per-device ring, one counter per launch
-// (zeroed on the launch stream), so concurrent launches on different streams do
-// not share a counter unless more than kCounters are in flight.
-constexpr int kCounters = 4096;
-std::mutex g_ctr_mu;
-std::map<int, std::pair<int*, unsigned>> g_ctr;
-
-int next_counter(int** out) {
-    int dev = 0;
-    GNA_CUDA_TRY(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(g_ctr_mu);
-    auto& e = g_ctr[dev];
-    if (!e.first) GNA_CUDA_TRY(cudaMalloc(&e.first, kCounters * sizeof(int)));
-    *out = e.first + (e.second++ % kCounters);
-    return GNA_OK;
-}
-
-// Attention kernel selection (GNA_KERNEL): "v3" (default: one CTA per work item of two
-// 128-row sub-tiles, attn_sm100.cu), "v3p" (v3 with the persistent work queue), "v4"
-// (experimental persistent single-sub-tile kernel, attn_v4.cu).  Measured on B200
-// (profiles/r01_v4_ab.txt): v4 moves 4x the L2 bytes of v3 (K/V reused by 128 rows instead
-// of 256) and its two key-half softmax warps per SMSP run in lockstep, so it is 1.4-2x slower.
-int kernel_choice() {
-    const char* v = getenv("GNA_KERNEL");
-    if (v && strcmp(v, "v4") == 0) return 4;
-    if (v && strcmp(v, "v3p") == 0) return 2;
-    return 3;
-}
-
-bool use_persistent() {
-    // default off (measured 12-25% slower on every config, profiles/r01_p1_ab_persistent.txt);
-    // GNA_PERSISTENT=1 selects the persistent work-queue kernel for A/B
-    const char* v = getenv("GNA_PERSISTENT");
-    return v && v[0] == '1';
-}
-
-// per-device copy of the work list
-int plan_device_items(Plan& p, int4** out) {
-    int dev = 0;
-    GNA_CUDA_TRY(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(p.mu);
-    auto it = p.dev_items.find(dev);
-    if (it != p.dev_items.end()) {
-        *out = it->second;
-        return GNA_OK;
-    }
-    // [items: n int4] then [info: 3 int4 per item] = {lo0, lo1, lo2, nkv}, {ext0, ext1, ext2, 0},
-    // {class coords c0, c1, c2, 0}: the union KV box range of the item's sub-tiles, decoded once on
-    // the host so the kernel's prologue has no integer divisions before its first TMA load
+// Host side of the work list: [items: n int4] then [info: 3 int4 per item] = {lo0, lo1, lo2, nkv},
+// {ext0, ext1, ext2, 0}, {class coords c0, c1, c2, 0}: the union KV box range of the item's
+// sub-tiles, decoded once on the host so the kernel's prologue has no integer divisions before
+// its first TMA load.  Kept in pinned memory for the lifetime of the plan (async upload source).
+int plan_host_items(Plan& p) {
+    if (p.host_items) return GNA_OK;
     const size_t n = p.items.size();
-    std::vector<int4> buf(std::max<size_t>(1, 4 * n));
+    const size_t count = std::max<size_t>(1, 4 * n);
+    int4* h = nullptr;
+    GNA_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h), count * sizeof(int4), cudaHostAllocPortable));
+    memset(h, 0, count * sizeof(int4));
     for (size_t i = 0; i < n; ++i) {
         const int4 it = p.items[i];
         int lo[3], hi[3];
@@ -425,16 +396,59 @@ int plan_device_items(Plan& p, int4** out) {
         }
         int cc[3];
         class_coords(p.g, it.x, cc);
-        buf[i] = it;
-        buf[n + 3 * i] = make_int4(lo[0], lo[1], lo[2], (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]));
-        buf[n + 3 * i + 1] = make_int4(hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 0);
-        buf[n + 3 * i + 2] = make_int4(cc[0], cc[1], cc[2], 0);
+        h[i] = it;
+        h[n + 3 * i] = make_int4(lo[0], lo[1], lo[2], (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]));
+        h[n + 3 * i + 1] = make_int4(hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 0);
+        h[n + 3 * i + 2] = make_int4(cc[0], cc[1], cc[2], 0);
     }
-    int4* d = nullptr;
-    GNA_CUDA_TRY(cudaMalloc(&d, buf.size() * sizeof(int4)));
-    GNA_CUDA_TRY(cudaMemcpy(d, buf.data(), buf.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    p.dev_items[dev] = d;
-    *out = d;
+    p.host_items = h;
+    p.host_count = count;
+    return GNA_OK;
+}
+
+bool stream_capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
+// Device work list for the current device, ordered before the caller's launch on `st`.
+// First use on a device: one cudaMalloc and an async H2D copy on `st` (no host sync).
+int plan_device_items(Plan& p, cudaStream_t st, int4** out) {
+    int dev = 0;
+    GNA_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(p.mu);
+    int rc = plan_host_items(p);
+    if (rc) return rc;
+    const bool capturing = stream_capturing(st);
+    auto it = p.dev_items.find(dev);
+    if (it == p.dev_items.end()) {
+        if (capturing)
+            return fail(GNA_EINVAL,
+                        "first call for this problem on this device is inside a CUDA graph capture: "
+                        "call it once before capturing (the work list upload allocates device memory)");
+        DevItems d;
+        GNA_CUDA_TRY(cudaMalloc(&d.ptr, p.host_count * sizeof(int4)));
+        GNA_CUDA_TRY(cudaMemcpyAsync(d.ptr, p.host_items, p.host_count * sizeof(int4), cudaMemcpyHostToDevice, st));
+        GNA_CUDA_TRY(cudaEventCreateWithFlags(&d.ready, cudaEventDisableTiming));
+        GNA_CUDA_TRY(cudaEventRecord(d.ready, st));
+        it = p.dev_items.emplace(dev, d).first;
+        *out = d.ptr;
+        return GNA_OK;
+    }
+    DevItems& d = it->second;
+    if (!d.done) {
+        if (capturing) {
+            // a capture cannot wait on an event recorded outside it: the upload is a few KB
+            // enqueued earlier, wait for it on the host once
+            GNA_CUDA_TRY(cudaEventSynchronize(d.ready));
+            d.done = true;
+        } else if (cudaEventQuery(d.ready) == cudaSuccess) {
+            d.done = true;
+        } else {
+            GNA_CUDA_TRY(cudaStreamWaitEvent(st, d.ready, 0));
+        }
+    }
+    *out = d.ptr;
     return GNA_OK;
 }
 
@@ -458,12 +472,19 @@ WsLayout ws_layout(const Geometry& g) {
     return L;
 }
 
+// Library-owned workspace cache, one buffer per (device, stream): concurrent calls on
+// different streams never share permuted buffers.  Growth is stream-ordered
+// (cudaMallocAsync on the calling stream, no device synchronisation); the outgrown buffer is
+// retired, not freed, so work still queued -- or a CUDA graph captured earlier -- that points
+// at it stays valid until gna_release_workspace().  Growth inside a stream capture is refused
+// (pass a caller workspace, or call once before capturing).
 struct DevWs {
     void* ptr = nullptr;
     size_t bytes = 0;
 };
 std::mutex g_ws_mu;
-std::map<int, DevWs> g_ws;
+std::map<std::pair<int, cudaStream_t>, DevWs> g_ws;
+std::map<int, std::vector<void*>> g_ws_retired;
 
 int get_workspace(const gna_args* a, size_t need, uint8_t** base) {
     if (a->workspace) {
@@ -474,17 +495,18 @@ int get_workspace(const gna_args* a, size_t need, uint8_t** base) {
     }
     int dev = 0;
     GNA_CUDA_TRY(cudaGetDevice(&dev));
+    cudaStream_t st = static_cast<cudaStream_t>(a->stream);
     std::lock_guard<std::mutex> lk(g_ws_mu);
-    DevWs& w = g_ws[dev];
+    DevWs& w = g_ws[{dev, st}];
     if (w.bytes < need) {
-        if (w.ptr) {
-            // a buffer still in use by queued work must not be freed early
-            GNA_CUDA_TRY(cudaDeviceSynchronize());
-            GNA_CUDA_TRY(cudaFree(w.ptr));
-            w.ptr = nullptr;
-            w.bytes = 0;
-        }
-        GNA_CUDA_TRY(cudaMalloc(&w.ptr, need));
+        if (stream_capturing(st))
+            return fail(GNA_EINVAL,
+                        "library workspace would grow inside a CUDA graph capture: pass gna_args.workspace "
+                        "(gna_workspace_size) or call once before capturing");
+        if (w.ptr) g_ws_retired[dev].push_back(w.ptr);
+        w.ptr = nullptr;
+        w.bytes = 0;
+        GNA_CUDA_TRY(cudaMallocAsync(&w.ptr, need, st));
         w.bytes = need;
     }
     *base = static_cast<uint8_t*>(w.ptr);
@@ -569,6 +591,21 @@ int make_tmap_extra(CUtensorMap* m, const void* base, const Geometry& g, int n_e
     return GNA_OK;
 }
 
+// SM count of the current device (cached per device id)
+int device_sms() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    cache[dev] = sms;
+    return sms;
+}
+
 int check_device() {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -621,7 +658,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
                  const CUtensorMap* direct_maps = nullptr) {
     int rc;
     int4* items = nullptr;
-    if ((rc = plan_device_items(*c.plan, &items))) return rc;
+    if ((rc = plan_device_items(*c.plan, c.st, &items))) return rc;
     CUtensorMap tq, tk, tv;
     if (direct) {
         tq = direct_maps[0];
@@ -644,37 +681,30 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.direct = direct ? 1 : 0;
     p.n_extra = a->n_extra > 0 ? a->n_extra : 0;
     p.extra_stages = (p.n_extra + 127) / 128;
-    p.sched_counter = nullptr;
     const bool fp8 = a->dtype == GNA_DTYPE_FP8_E4M3;
-    const int kc = fp8 ? 3 : kernel_choice();  // the E4M3 path exists in the v3 kernel only
-    if ((kc == 2 || (kc == 3 && use_persistent())) && (rc = next_counter(&p.sched_counter))) return rc;
     p.g = c.g;
     p.items = items;
     p.n_items = static_cast<long long>(c.plan->items.size());
     p.item_info = items + p.n_items;
     const long long total = p.n_items * a->batch * a->heads;
-    long long wb = a->work_begin, we = a->work_end;
-    if (we <= 0 || we > total) we = total;
-    if (wb < 0) wb = 0;
-    if (wb > we) return fail(GNA_EINVAL, "work_begin > work_end");
+    long long wb = 0, we = total;
+    if (a->flags & GNA_FLAG_WORK_RANGE) {  // [work_begin, work_end) taken literally (may be empty)
+        wb = a->work_begin;
+        we = a->work_end;
+        if (wb < 0 || we > total || wb > we) return fail(GNA_EINVAL, "work range outside [0, n_work] or begin > end");
+    } else if (a->work_begin != 0 || a->work_end > 0) {  // legacy: end <= 0 means "to the end"
+        wb = a->work_begin;
+        if (a->work_end > 0) we = a->work_end;
+        if (wb < 0 || we > total || wb > we) return fail(GNA_EINVAL, "work range outside [0, n_work] or begin > end");
+    }
     p.work_begin = wb;
     p.work_end = we;
     p.o_perm = c.ws ? c.ws + c.L.o : nullptr;
-    p.q_src = direct ? a->q : (c.ws ? c.ws + c.L.q : nullptr);
     p.lse_perm = c.ws ? reinterpret_cast<float*>(c.ws + c.L.lse) : nullptr;
     const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));
     p.scale_log2 = scale * 1.4426950408889634f;
     p.fp8 = fp8 ? 1 : 0;
-    {
-        static int sms = 0;
-        if (sms == 0) {
-            int dev = 0;
-            if (cudaGetDevice(&dev) != cudaSuccess ||
-                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-                sms = 148;
-        }
-        p.num_sms = sms;
-    }
+    p.num_sms = device_sms();
     p.o_scale = 1.0f;
     if (fp8) {  // per-tensor dequantisation: S scales by q_scale*k_scale, O by v_scale
         p.scale_log2 *= (a->q_scale > 0.f ? a->q_scale : 1.f) * (a->k_scale > 0.f ? a->k_scale : 1.f);
@@ -685,7 +715,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     // v3 epilogue: O through smem and TMA stores (GNA_TMA_STORE=0 keeps per-thread stores)
     p.tma_store = 0;
     const char* ts_env = getenv("GNA_TMA_STORE");
-    if (kc == 3 && !(ts_env && ts_env[0] == '0')) {
+    if (!(ts_env && ts_env[0] == '0')) {
         // The 5-D map folds batch into axis 0, so a box (or a padding box of the sub-tile grid)
         // past the end of axis 0 would write into the next sample: only when the box grid tiles
         // axis 0 exactly (or batch == 1).
@@ -701,8 +731,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
             p.tma_store = 1;
         }
     }
-    if (kc == 4) GNA_CUDA_TRY(launch_attention_v4(p, tq, tk, tv, tek, tev, c.st));
-    else GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, tek, tev, we - wb, c.st));
+    GNA_CUDA_TRY(launch_attention(p, tq, tk, tv, tek, tev, we - wb, c.st));
     return post_launch(a, c.st, "gna_attn_sm100");
 }
 
@@ -888,14 +917,38 @@ int gna_debug_worklist(const gna_args* a, int32_t* host_out, long long* n_items)
 int gna_release_workspace(void) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return GNA_OK;
-    std::lock_guard<std::mutex> lk(g_ws_mu);
-    auto it = g_ws.find(dev);
-    if (it != g_ws.end() && it->second.ptr) {
-        cudaError_t e = cudaDeviceSynchronize();
-        if (e == cudaSuccess) e = cudaFree(it->second.ptr);
-        it->second = DevWs{};
-        if (e != cudaSuccess) return fail(GNA_ECUDA, cudaGetErrorString(e));
+    // everything queued on the device may still read these buffers
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return fail(GNA_ECUDA, cudaGetErrorString(e));
+    {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        for (auto it = g_ws.begin(); it != g_ws.end();) {
+            if (it->first.first == dev) {
+                if (it->second.ptr) cudaFree(it->second.ptr);
+                it = g_ws.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        for (void* ptr : g_ws_retired[dev]) cudaFree(ptr);
+        g_ws_retired.erase(dev);
     }
+    {
+        // device work lists of every cached plan on this device (re-uploaded on next use)
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        for (auto& kv : g_plans) {
+            Plan& p = *kv.second;
+            std::lock_guard<std::mutex> lk2(p.mu);
+            auto it = p.dev_items.find(dev);
+            if (it != p.dev_items.end()) {
+                cudaFree(it->second.ptr);
+                if (it->second.ready) cudaEventDestroy(it->second.ready);
+                p.dev_items.erase(it);
+            }
+        }
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(GNA_ECUDA, cudaGetErrorString(e));
     return GNA_OK;
 }
 

@@ -1,5 +1,4 @@
-// attn_common.cuh -- helpers shared by the attention kernels (attn_sm100.cu,
-// attn_v4.cu): trace macros, compile-time variant knobs, stage decoding and
+// attn_common.cuh -- helpers of the attention kernel (attn_sm100.cu): trace macros, compile-time variant knobs, stage decoding and
 // the separable GNA row mask over a box (P:627-628 fine-grained masking).
 #pragma once
 #include <cuda.h>

@@ -32,6 +32,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "geom.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
@@ -707,43 +709,25 @@ __global__ void __launch_bounds__(384, 1)
     }
 }
 
-#include "attn_persistent.cuh"
-
+// The dynamic-smem opt-in is a per-device (per-context) attribute: it is recorded per
+// device id, so a process driving several GPUs configures each before its first launch.
 template <int DP, int BV, bool F8 = false>
 static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
                             cudaStream_t stream) {
     using C = Cfg<DP, BV, F8>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gna_attn_sm100<DP, BV, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             C::SMEM_BYTES);
+    constexpr int kMaxDev = 64;
+    static std::atomic<unsigned char> configured[kMaxDev];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDev || !configured[dev].load(std::memory_order_acquire)) {
+        e = cudaFuncSetAttribute(gna_attn_sm100<DP, BV, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM_BYTES);
         if (e != cudaSuccess) return e;
-        configured = true;
+        if (dev >= 0 && dev < kMaxDev) configured[dev].store(1, std::memory_order_release);
     }
     if (n_ctas <= 0) return cudaSuccess;
-    if constexpr (!F8) if (p.sched_counter != nullptr) {
-        static bool pconfigured = false;
-        if (!pconfigured) {
-            cudaError_t e = cudaFuncSetAttribute(gna_attn_sm100_persistent<DP, BV>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-            if (e != cudaSuccess) return e;
-            pconfigured = true;
-        }
-        static int sms = 0;
-        if (sms == 0) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (sms <= 0) sms = 148;
-        }
-        const long long grid = n_ctas < sms ? n_ctas : sms;
-        cudaError_t e = cudaMemsetAsync(p.sched_counter, 0, sizeof(int), stream);
-        if (e != cudaSuccess) return e;
-        gna_attn_sm100_persistent<DP, BV>
-            <<<static_cast<unsigned>(grid), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
-        return cudaGetLastError();
-    }
     gna_attn_sm100<DP, BV, F8><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
     return cudaGetLastError();
 }
@@ -753,7 +737,7 @@ cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const C
                              cudaStream_t stream) {
     const int dp = p.g.Dp, bv = p.g.box_vol;
     if (p.fp8) {
-        if (p.sched_counter != nullptr || dp != 128) return cudaErrorInvalidValue;
+        if (dp != 128) return cudaErrorInvalidValue;
         if (bv == 128) return launch_t<128, 128, true>(p, tq, tk, tv, tek, tev, n_ctas, stream);
         if (bv == 64) return launch_t<128, 64, true>(p, tq, tk, tv, tek, tev, n_ctas, stream);
         return cudaErrorInvalidValue;

@@ -22,8 +22,6 @@ struct AttnParams {
     int direct;             // 1: Q/K/V tensor maps are 5-D maps over the user tensors (no permute pass)
     int n_extra;            // extra (text) KV tokens per (batch, head), appended as dense stages
     int extra_stages;       // ceil(n_extra / 128)
-    int* sched_counter;     // non-null: persistent kernel with a dynamic work queue (zeroed per launch)
-    const void* q_src;      // v4: Q rows read by the epilogue warpgroup (direct: user q; else permuted q)
     void* out_nat;          // if non-null: fused inverse permutation, O written to the user layout
     float* lse_nat;         //   and LSE likewise (may be null)
     // O written by TMA stores from smem (v3): 0 = per-thread stores, 1 = 2-D map over the
@@ -43,11 +41,6 @@ inline long long perm_rows(const Geometry& g) {
 cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                              const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
                              cudaStream_t stream);
-
-// persistent kernel (attn_v4.cu): one CTA per SM, tasks = 128-row Q sub-tiles of the work range
-cudaError_t launch_attention_v4(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
-                                const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev,
-                                cudaStream_t stream);
 
 // q/k/v natural [B][s0][s1][s2][H][D] -> permuted [BH][C][nbox][box_vol][Dp]
 cudaError_t launch_permute_qkv(const Geometry& g, const void* q, const void* k, const void* v, void* qp,

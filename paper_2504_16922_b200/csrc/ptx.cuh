@@ -403,12 +403,15 @@ __device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, 
 }
 // 2^x for a pair on the FMA/ALU pipes (offloads the MUFU unit): round-to-nearest
 // split x = n + f, f in [-0.5, 0.5], degree-3 minimax polynomial for 2^f (max rel.
-// error 7.5e-5, far below bf16's 2^-9), exponent added as n << 23.  x is clamped to
-// >= -126 so the result stays a (tiny) positive float; the caller keeps x <= 8.
-__device__ __forceinline__ void ex2_poly2(float& y0, float& y1, float x0, float x1) {
+// error 7.5e-5, far below bf16's 2^-9), exponent added as n << 23.  The polynomial
+// runs on x clamped to >= -126 (so the exponent add stays in range) and the result is
+// then selected to exactly 0 for x < -126 -- in particular for masked logits (x = -inf),
+// like ex2.approx.ftz, so a masked key never reaches O even if its V row holds inf/NaN or
+// a huge value.  The caller keeps x <= 8.
+__device__ __forceinline__ void ex2_poly2(float& y0, float& y1, float x0_in, float x1_in) {
     const float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic holds round(x) in the low bits
-    x0 = fmaxf(x0, -126.0f);
-    x1 = fmaxf(x1, -126.0f);
+    const float x0 = fmaxf(x0_in, -126.0f);
+    const float x1 = fmaxf(x1_in, -126.0f);
     float t0, t1, r0, r1, f0, f1, q0, q1;
     fadd2(t0, t1, x0, x1, kMagic, kMagic);
     fadd2(r0, r1, t0, t1, -kMagic, -kMagic);
@@ -418,6 +421,8 @@ __device__ __forceinline__ void ex2_poly2(float& y0, float& y1, float x0, float 
     ffma2(q0, q1, q0, q1, f0, f1, 0.99992818f, 0.99992818f);
     y0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
     y1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+    y0 = x0_in < -126.0f ? 0.0f : y0;
+    y1 = x1_in < -126.0f ? 0.0f : y1;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

@@ -22,6 +22,7 @@ GNA_DTYPE_FP8_E4M3 = 2
 GNA_FLAG_SYNC_CHECK = 1
 GNA_FLAG_UNFUSED_EPILOGUE = 2
 GNA_FLAG_PERMUTED = 4
+GNA_FLAG_WORK_RANGE = 8
 
 _I3 = ctypes.c_int * 3
 
@@ -120,7 +121,8 @@ def make_args(batch, heads, head_dim, spatial, window, stride=None, dilation=Non
     a.workspace_bytes = int(workspace_bytes)
     a.box = _I3(*(_pad3(box, 1) if box else [0, 0, 0]))
     a.work_begin, a.work_end = (work_range if work_range is not None else (0, 0))
-    a.flags = int(flags)
+    # an explicit range is taken literally (an empty share launches nothing)
+    a.flags = int(flags) | (GNA_FLAG_WORK_RANGE if work_range is not None else 0)
     a.extra_k, a.extra_v, a.n_extra = extra_k, extra_v, int(n_extra)
     return a
 
@@ -138,8 +140,20 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
             raise GnaError(f"{name} must be {want} (q, k, v all bfloat16, or all float8_e4m3fn with a bfloat16 out)")
         if not t.is_contiguous():
             raise GnaError(f"{name} must be contiguous")
-    if lse is not None and (lse.dtype != torch.float32 or not lse.is_contiguous()):
-        raise GnaError("lse must be contiguous float32")
+    if lse is not None and (lse.dtype != torch.float32 or not lse.is_contiguous() or not lse.is_cuda):
+        raise GnaError("lse must be a contiguous CUDA float32 tensor")
+    # the kernels index k, v, out and lse with q's geometry: any mismatch would read or write
+    # out of bounds, so it is rejected here (nothing is launched)
+    if not 4 <= q.dim() <= 6:
+        raise GnaError("q must be [B, *spatial (1-3 axes), H, D]")
+    for name, t in (("k", k), ("v", v), ("out", out)):
+        if tuple(t.shape) != tuple(q.shape):
+            raise GnaError(f"{name} shape {tuple(t.shape)} != q shape {tuple(q.shape)}")
+    if lse is not None and tuple(lse.shape) != tuple(q.shape[:-1]):
+        raise GnaError(f"lse shape {tuple(lse.shape)} != {tuple(q.shape[:-1])}")
+    devs = {t.device for t in (q, k, v, out) + ((lse,) if lse is not None else ())}
+    if len(devs) != 1:
+        raise GnaError(f"all tensors must be on one CUDA device, got {sorted(map(str, devs))}")
     batch, heads, head_dim = q.shape[0], q.shape[-2], q.shape[-1]
     spatial = list(q.shape[1:-2])
     if stream is None:
@@ -158,6 +172,8 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
         if extra_k.shape != extra_v.shape or extra_k.dim() != 4 or extra_k.shape[0] != batch or \
                 tuple(extra_k.shape[2:]) != (heads, head_dim):
             raise GnaError("extra_k/extra_v must be [B, T, H, D] matching q")
+        if extra_k.device != q.device or extra_v.device != q.device:
+            raise GnaError("extra_k/extra_v must be on q's device")
         ek, ev, n_extra = extra_k.data_ptr(), extra_v.data_ptr(), extra_k.shape[1]
     return make_args(batch, heads, head_dim, spatial, window, stride, dilation, causal, scale,
                      q=q.data_ptr(), k=k.data_ptr(), v=v.data_ptr(), out=out.data_ptr(),

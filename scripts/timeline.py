@@ -17,7 +17,7 @@ w = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2b_flux64_s16"]
 f = w.full()
 q, k, v = (t.cuda() for t in make_qkv(w.batch, w.spatial, w.heads, w.head_dim))
 lib = gna.load()
-V4 = os.environ.get("GNA_KERNEL", "v4") == "v4"
+V4 = False  # the v4 kernel was removed in round 2
 if V4:
     lib.gna_debug_trace_reset = lib.gna_debug_timeline_v4_reset
     lib.gna_debug_timeline = lib.gna_debug_timeline_v4

@@ -324,16 +324,3 @@ def test_tma_store_epilogue_bitwise(gna, cfg, monkeypatch):
         res[ts] = (o, l, o2, l2)
     for a, b in zip(res["0"], res["1"]):
         assert torch.equal(a, b)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("kernel", ["v3p", "v4"])
-@pytest.mark.parametrize("cfg", [SMALL[1], SMALL[2], SMALL[4], SMALL[6]], ids=_ids)
-def test_alternative_kernels_vs_oracle(gna, cfg, kernel, monkeypatch):
-    """The A/B kernels kept in the tree (GNA_KERNEL=v3p persistent work queue, GNA_KERNEL=v4
-    persistent single-sub-tile kernel) stay correct against the oracle."""
-    monkeypatch.setenv("GNA_KERNEL", kernel)
-    B, H, D = 2, 2, 128
-    (q, k, v), o, l = _run(gna, cfg, B, H, D, True)
-    ro, rl = O.forward(as_f32_numpy(q), as_f32_numpy(k), as_f32_numpy(v), O.Params(**cfg))
-    _assert_close(o, ro, l, rl)
