@@ -22,7 +22,7 @@
  *   out[q] = softmax_k(scale * q.k) v,   lse[q] = ln sum_k exp(scale * q.k).
  *
  * Layout (a build decision -- the paper states none; heads-last as NATTEN):
- *   q, k, v, out : bf16 [batch][s0][s1][s2][heads][head_dim], contiguous
+ *   q, k, v, out : bf16 (or fp16) [batch][s0][s1][s2][heads][head_dim], contiguous
  *                  (GNA_DTYPE_FP8_E4M3: q, k, v are E4M3 bytes, same shape; out stays bf16)
  *   lse          : fp32 [batch][s0][s1][s2][heads]
  *   1-D problems pass spatial = {L, 1, 1}; unused axes must be exactly
@@ -90,6 +90,10 @@ extern "C" {
 #define GNA_ENOMEM 4
 
 #define GNA_DTYPE_BF16 0
+/* fp16 Q/K/V and fp16 O (fp32 LSE): the precision of every throughput the paper quotes
+ * (P:69-70).  Same kernels as bf16 with kind::f16 F16 operands; P is packed
+ * to fp16 (P <= 2^8 by the lazy running max) before PV.  Every route and the stage API. */
+#define GNA_DTYPE_FP16 1
 /* E4M3 Q/K/V with per-tensor scales (gna_args.q_scale/k_scale/v_scale: real value =
  * stored value x scale), bf16 O and fp32 LSE -- the FP8 forward the paper quotes for its
  * Blackwell kernel.  QK^T and PV run as E4M3
@@ -111,13 +115,13 @@ extern "C" {
                                         {0, 0} (a zero-initialised struct) means all work items */
 
 typedef struct gna_args {
-    const void *q, *k, *v; /* device bf16 [B][s0][s1][s2][H][D] */
-    void *out;             /* device bf16, same shape */
+    const void *q, *k, *v; /* device bf16/fp16/E4M3 [B][s0][s1][s2][H][D] (see dtype) */
+    void *out;             /* device, same shape: fp16 for GNA_DTYPE_FP16, else bf16 */
     float *lse;            /* device fp32 [B][s0][s1][s2][H]; may be NULL */
     int batch, heads, head_dim;
     int spatial[3], window[3], stride[3], dilation[3], causal[3];
     float scale;            /* <= 0 -> 1/sqrt(head_dim) */
-    int dtype;              /* GNA_DTYPE_BF16 or GNA_DTYPE_FP8_E4M3 (q, k, v; out stays bf16) */
+    int dtype;              /* GNA_DTYPE_BF16, GNA_DTYPE_FP16 or GNA_DTYPE_FP8_E4M3 */
     void *stream;           /* cudaStream_t */
     void *workspace;        /* optional caller workspace (device, 256-B aligned) */
     size_t workspace_bytes;
@@ -130,9 +134,10 @@ typedef struct gna_args {
                                [0, n_work] or begin > end: GNA_EINVAL. */
     int flags;
     /* Extra (text) KV tokens fused into the same kernel:
-     * n_extra keys/values per (batch, head), layout bf16 [B][n_extra][H][D],
-     * attended densely by EVERY query in the same softmax as its GNA
-     * neighbourhood.  0 / NULL = none.  Requires head_dim >= 64. */
+     * n_extra keys/values per (batch, head), layout [B][n_extra][H][D] in q's
+     * 16-bit dtype (bf16 or fp16), attended densely by EVERY query in the same
+     * softmax as its GNA neighbourhood.  0 / NULL = none.  Requires
+     * head_dim >= 64. */
     const void *extra_k, *extra_v;
     int n_extra;
     /* GNA_DTYPE_FP8_E4M3 only: per-tensor dequantisation scales (<= 0 -> 1). */

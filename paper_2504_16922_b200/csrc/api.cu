@@ -61,8 +61,8 @@ int pow2ceil(int x) { return 1 << ilog2(x < 1 ? 1 : x); }
 // --------------------------------------------------------------- validation
 int validate(const gna_args* a, bool need_ptrs) {
     if (!a) return fail(GNA_EINVAL, "args is NULL");
-    if (a->dtype != GNA_DTYPE_BF16 && a->dtype != GNA_DTYPE_FP8_E4M3)
-        return fail(GNA_EUNSUPPORTED, "dtype: GNA_DTYPE_BF16 or GNA_DTYPE_FP8_E4M3");
+    if (a->dtype != GNA_DTYPE_BF16 && a->dtype != GNA_DTYPE_FP16 && a->dtype != GNA_DTYPE_FP8_E4M3)
+        return fail(GNA_EUNSUPPORTED, "dtype: GNA_DTYPE_BF16, GNA_DTYPE_FP16 or GNA_DTYPE_FP8_E4M3");
     if (a->dtype == GNA_DTYPE_FP8_E4M3) {
         if (a->head_dim != 128) return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 needs head_dim 128");
         if (a->n_extra > 0) return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 with extra KV tokens is not supported");
@@ -531,7 +531,12 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
-int make_tmap(CUtensorMap* m, const void* base, const Geometry& g) {
+// TMA element type of the 16-bit tensors of a call (Q/K/V/O for bf16 / fp16, O for E4M3)
+CUtensorMapDataType tmap_dtype16(int dtype) {
+    return dtype == GNA_DTYPE_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+}
+
+int make_tmap(CUtensorMap* m, const void* base, const Geometry& g, CUtensorMapDataType dt) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled unavailable");
     const long long rows = perm_rows(g);
@@ -540,7 +545,7 @@ int make_tmap(CUtensorMap* m, const void* base, const Geometry& g) {
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.Dp) * 2};
     cuuint32_t box[2] = {64, static_cast<cuuint32_t>(g.box_vol)};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+    CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
@@ -550,7 +555,8 @@ int make_tmap(CUtensorMap* m, const void* base, const Geometry& g) {
 // 5-D map over a user tensor [B][s0][s1][s2][H][D] (direct, permute-free mode):
 // dims (D, H, s2, s1, B*s0), box {64, 1, B2*d2, B1*d1, B0*d0}, element strides
 // (1, 1, d2, d1, d0): one box load gathers the box of one dilation class of one head.
-int make_tmap_direct(CUtensorMap* m, const void* base, const Geometry& g, bool* ok, int elem_bytes = 2) {
+int make_tmap_direct(CUtensorMap* m, const void* base, const Geometry& g, bool* ok, CUtensorMapDataType dt) {
+    const int elem_bytes = dt == CU_TENSOR_MAP_DATA_TYPE_UINT8 ? 1 : 2;
     *ok = false;
     EncodeTiledFn enc = get_encode();
     if (!enc) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled unavailable");
@@ -567,7 +573,7 @@ int make_tmap_direct(CUtensorMap* m, const void* base, const Geometry& g, bool* 
     cuuint32_t estr[5] = {1, 1, static_cast<cuuint32_t>(g.ax[2].d), static_cast<cuuint32_t>(g.ax[1].d),
                           static_cast<cuuint32_t>(g.ax[0].d)};
     if (dims[4] >= (1ull << 31)) return GNA_OK;
-    CUresult r = enc(m, elem_bytes == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5,
+    CUresult r = enc(m, dt, 5,
                      const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -576,7 +582,7 @@ int make_tmap_direct(CUtensorMap* m, const void* base, const Geometry& g, bool* 
 }
 
 // 3-D map over extra KV [B][T][H][D]: dims (D, H, B*T), box {64, 1, 128 tokens}.
-int make_tmap_extra(CUtensorMap* m, const void* base, const Geometry& g, int n_extra) {
+int make_tmap_extra(CUtensorMap* m, const void* base, const Geometry& g, int n_extra, CUtensorMapDataType dt) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t D = g.D, H = g.heads;
@@ -584,7 +590,7 @@ int make_tmap_extra(CUtensorMap* m, const void* base, const Geometry& g, int n_e
     cuuint64_t strides[2] = {D * 2, H * D * 2};
     cuuint32_t box[3] = {64, 1, 128};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+    CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(GNA_ECUDA, "cuTensorMapEncodeTiled (extra KV) failed: " + std::to_string(r));
@@ -658,6 +664,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
                  const CUtensorMap* direct_maps = nullptr) {
     int rc;
     int4* items = nullptr;
+    const CUtensorMapDataType dt16 = tmap_dtype16(a->dtype);
     if ((rc = plan_device_items(*c.plan, c.st, &items))) return rc;
     CUtensorMap tq, tk, tv;
     if (direct) {
@@ -665,17 +672,17 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
         tk = direct_maps[1];
         tv = direct_maps[2];
     } else {
-        if ((rc = make_tmap(&tq, c.ws + c.L.q, c.g))) return rc;
-        if ((rc = make_tmap(&tk, c.ws + c.L.k, c.g))) return rc;
-        if ((rc = make_tmap(&tv, c.ws + c.L.v, c.g))) return rc;
+        if ((rc = make_tmap(&tq, c.ws + c.L.q, c.g, dt16))) return rc;
+        if ((rc = make_tmap(&tk, c.ws + c.L.k, c.g, dt16))) return rc;
+        if ((rc = make_tmap(&tv, c.ws + c.L.v, c.g, dt16))) return rc;
     }
     CUtensorMap tek, tev;
     memset(&tek, 0, sizeof tek);
     memset(&tev, 0, sizeof tev);
     if (a->n_extra > 0) {
         if (!a->extra_k || !a->extra_v) return fail(GNA_EINVAL, "extra_k/extra_v NULL with n_extra > 0");
-        if ((rc = make_tmap_extra(&tek, a->extra_k, c.g, a->n_extra))) return rc;
-        if ((rc = make_tmap_extra(&tev, a->extra_v, c.g, a->n_extra))) return rc;
+        if ((rc = make_tmap_extra(&tek, a->extra_k, c.g, a->n_extra, dt16))) return rc;
+        if ((rc = make_tmap_extra(&tev, a->extra_v, c.g, a->n_extra, dt16))) return rc;
     }
     AttnParams p{};
     p.direct = direct ? 1 : 0;
@@ -704,6 +711,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf(static_cast<float>(a->head_dim));
     p.scale_log2 = scale * 1.4426950408889634f;
     p.fp8 = fp8 ? 1 : 0;
+    p.fp16 = a->dtype == GNA_DTYPE_FP16 ? 1 : 0;
     p.num_sms = device_sms();
     p.o_scale = 1.0f;
     if (fp8) {  // per-tensor dequantisation: S scales by q_scale*k_scale, O by v_scale
@@ -724,10 +732,10 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
         const bool tiles_axis0 = a->batch == 1 || c.g.nb[0] * c.g.B[0] == c.g.ax[0].L;  // no padded boxes
         if (fused_out) {
             bool ok = false;
-            if (!dilated && tiles_axis0 && (rc = make_tmap_direct(&p.tmap_o, a->out, c.g, &ok))) return rc;
+            if (!dilated && tiles_axis0 && (rc = make_tmap_direct(&p.tmap_o, a->out, c.g, &ok, dt16))) return rc;
             p.tma_store = ok ? 2 : 0;
         } else if (c.ws) {
-            if ((rc = make_tmap(&p.tmap_o, c.ws + c.L.o, c.g))) return rc;
+            if ((rc = make_tmap(&p.tmap_o, c.ws + c.L.o, c.g, dt16))) return rc;
             p.tma_store = 1;
         }
     }
@@ -758,10 +766,10 @@ int gna_forward_ex(const gna_args* a) {
         // O and LSE scattered by the epilogue
         CUtensorMap maps[3];
         bool ok[3];
-        const int eb = fp8 ? 1 : 2;
-        if ((rc = make_tmap_direct(&maps[0], a->q, c.g, &ok[0], eb))) return rc;
-        if ((rc = make_tmap_direct(&maps[1], a->k, c.g, &ok[1], eb))) return rc;
-        if ((rc = make_tmap_direct(&maps[2], a->v, c.g, &ok[2], eb))) return rc;
+        const CUtensorMapDataType dt = fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : tmap_dtype16(a->dtype);
+        if ((rc = make_tmap_direct(&maps[0], a->q, c.g, &ok[0], dt))) return rc;
+        if ((rc = make_tmap_direct(&maps[1], a->k, c.g, &ok[1], dt))) return rc;
+        if ((rc = make_tmap_direct(&maps[2], a->v, c.g, &ok[2], dt))) return rc;
         if (ok[0] && ok[1] && ok[2]) return do_attention(a, c, /*fused_out=*/true, /*direct=*/true, maps);
         if (fp8) return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 needs the permute-free path (box*dilation <= 256, dilation <= 8)");
     }

@@ -72,13 +72,23 @@ namespace gna {
 
 namespace {
 using namespace attn;
+
+// O row element pair -> 16-bit output (bf16 for the bf16 and E4M3 inputs, fp16 for fp16)
+template <bool F16>
+__device__ __forceinline__ uint32_t pack_o(float lo, float hi) {
+    if constexpr (F16) return ptx::pack_f16x2(lo, hi);
+    else return ptx::pack_bf16x2(lo, hi);
+}
 }  // namespace
 
-template <int DP, int BV, bool F8>
+// DT: element type of Q/K/V (and O for the 16-bit types): 0 bf16, 1 fp16, 2 E4M3 (O bf16)
+template <int DP, int BV, int DT>
 __global__ void __launch_bounds__(384, 1)
     gna_attn_sm100(const __grid_constant__ AttnParams p, const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                    const __grid_constant__ CUtensorMap tmap_ek, const __grid_constant__ CUtensorMap tmap_ev) {
+    constexpr bool F8 = DT == 2;
+    constexpr bool F16 = DT == 1;
     using C = Cfg<DP, BV, F8>;
     constexpr int KPB = C::KPB;
     static_assert(!F8 || (DP == 128 && GNA_PSPLIT <= 2), "E4M3 path: head_dim 128, P split 1 or 2");
@@ -299,8 +309,12 @@ __global__ void __launch_bounds__(384, 1)
         // warp-uniform: all lanes run the loop, one elected lane issues each tcgen05 op, so
         // descriptors stay in uniform registers (GNA_V3_ELECT=0: lane 0 only, for A/B)
         if (GNA_V3_ELECT || lane == 0) {
-            constexpr uint32_t IDESC_QK = F8 ? ptx::idesc_e4m3(128, 128, 0, 0) : ptx::idesc_bf16(128, 128, 0, 0);
-            constexpr uint32_t IDESC_PV = F8 ? ptx::idesc_e4m3(128, DP, 0, 1) : ptx::idesc_bf16(128, DP, 0, 1);
+            constexpr uint32_t IDESC_QK = F8    ? ptx::idesc_e4m3(128, 128, 0, 0)
+                                          : F16 ? ptx::idesc_f16(128, 128, 0, 0)
+                                                : ptx::idesc_bf16(128, 128, 0, 0);
+            constexpr uint32_t IDESC_PV = F8    ? ptx::idesc_e4m3(128, DP, 0, 1)
+                                          : F16 ? ptx::idesc_f16(128, DP, 0, 1)
+                                                : ptx::idesc_bf16(128, DP, 0, 1);
             constexpr int KQ = DP / C::KSTEP;   // QK^T instructions (K = head_dim)
             constexpr int KP = 128 / C::KSTEP;  // PV instructions (K = 128 keys); P step = 8 TMEM columns
             constexpr uint32_t V_STEP = C::KSTEP * 128;  // bytes of V per K step (rows of 128 B)
@@ -514,6 +528,8 @@ __global__ void __launch_bounds__(384, 1)
                     const uint32_t h16 = ptx::pack_e4m3x2(y0, y1);  // P <= 2^8 by the lazy max: in range
                     if (pi & 1) pk[pi >> 1] |= h16 << 16;
                     else pk[pi >> 1] = h16;
+                } else if constexpr (F16) {
+                    pk[pi] = ptx::pack_f16x2(y0, y1);  // P <= 2^8 by the lazy max: in fp16 range
                 } else {
                     pk[pi] = ptx::pack_bf16x2(y0, y1);
                 }
@@ -606,7 +622,7 @@ __global__ void __launch_bounds__(384, 1)
         // Output row: the permuted O row (stage API), or -- fused inverse permutation
         // -- the row of this token in the user's heads-last
         // layout [B][s0][s1][s2][H][D], so no separate unpermute pass is needed.
-        __nv_bfloat16* orow;
+        __nv_bfloat16* orow;  // 16-bit rows (bf16 or fp16 bits)
         float* lrow;
         int ncols;
         if (p.out_nat != nullptr) {
@@ -640,7 +656,7 @@ __global__ void __launch_bounds__(384, 1)
                 uint32_t pk[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e)
-                    pk[e] = ptx::pack_bf16x2(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
+                    pk[e] = pack_o<F16>(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
                 const uint32_t rowb = sO + (c >> 1) * C::CHUNK_BYTES + r * 128;
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
@@ -683,7 +699,7 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t pk[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e)
-                pk[e] = ptx::pack_bf16x2(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
+                pk[e] = pack_o<F16>(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
             if (valid && c * 32 < ncols) {
                 uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
@@ -711,24 +727,24 @@ __global__ void __launch_bounds__(384, 1)
 
 // The dynamic-smem opt-in is a per-device (per-context) attribute: it is recorded per
 // device id, so a process driving several GPUs configures each before its first launch.
-template <int DP, int BV, bool F8 = false>
+template <int DP, int BV, int DT = 0>
 static cudaError_t launch_t(const AttnParams& p, const CUtensorMap& tq, const CUtensorMap& tk,
                             const CUtensorMap& tv, const CUtensorMap& tek, const CUtensorMap& tev, long long n_ctas,
                             cudaStream_t stream) {
-    using C = Cfg<DP, BV, F8>;
+    using C = Cfg<DP, BV, DT == 2>;
     constexpr int kMaxDev = 64;
     static std::atomic<unsigned char> configured[kMaxDev];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= kMaxDev || !configured[dev].load(std::memory_order_acquire)) {
-        e = cudaFuncSetAttribute(gna_attn_sm100<DP, BV, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(gna_attn_sm100<DP, BV, DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         if (dev >= 0 && dev < kMaxDev) configured[dev].store(1, std::memory_order_release);
     }
     if (n_ctas <= 0) return cudaSuccess;
-    gna_attn_sm100<DP, BV, F8><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
+    gna_attn_sm100<DP, BV, DT><<<static_cast<unsigned>(n_ctas), C::THREADS, C::SMEM_BYTES, stream>>>(p, tq, tk, tv, tek, tev);
     return cudaGetLastError();
 }
 
@@ -738,8 +754,15 @@ cudaError_t launch_attention(const AttnParams& p, const CUtensorMap& tq, const C
     const int dp = p.g.Dp, bv = p.g.box_vol;
     if (p.fp8) {
         if (dp != 128) return cudaErrorInvalidValue;
-        if (bv == 128) return launch_t<128, 128, true>(p, tq, tk, tv, tek, tev, n_ctas, stream);
-        if (bv == 64) return launch_t<128, 64, true>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+        if (bv == 128) return launch_t<128, 128, 2>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+        if (bv == 64) return launch_t<128, 64, 2>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+        return cudaErrorInvalidValue;
+    }
+    if (p.fp16) {
+        if (dp == 128 && bv == 128) return launch_t<128, 128, 1>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+        if (dp == 128 && bv == 64) return launch_t<128, 64, 1>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+        if (dp == 64 && bv == 128) return launch_t<64, 128, 1>(p, tq, tk, tv, tek, tev, n_ctas, stream);
+        if (dp == 64 && bv == 64) return launch_t<64, 64, 1>(p, tq, tk, tv, tek, tev, n_ctas, stream);
         return cudaErrorInvalidValue;
     }
     if (dp == 128 && bv == 128) return launch_t<128, 128>(p, tq, tk, tv, tek, tev, n_ctas, stream);

@@ -29,6 +29,7 @@ struct AttnParams {
     int tma_store;
     int num_sms;            // v3: the SM count (L2 prefetch of the next wave's Q boxes: CTA + num_sms)
     int fp8;                // 1: Q/K/V are E4M3, per-tensor scales folded in below
+    int fp16;               // 1: Q/K/V and O are fp16 (kind::f16 with F16 operands, P packed f16x2)
     float o_scale;          // O multiplier (v_scale for FP8, 1 for bf16)
     CUtensorMap tmap_o;
 };

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("GNA_LIB_PATH") or os.path.join(_HERE, "libgna_b200.so
 
 GNA_OK, GNA_EINVAL, GNA_EUNSUPPORTED, GNA_ECUDA, GNA_ENOMEM = range(5)
 GNA_DTYPE_BF16 = 0
+GNA_DTYPE_FP16 = 1
 GNA_DTYPE_FP8_E4M3 = 2
 GNA_FLAG_SYNC_CHECK = 1
 GNA_FLAG_UNFUSED_EPILOGUE = 2
@@ -132,12 +133,15 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
     import torch
 
     fp8 = q.dtype == torch.float8_e4m3fn
+    fp16 = q.dtype == torch.float16
+    t16 = torch.float16 if fp16 else torch.bfloat16  # O (and extra K/V) dtype
     for name, t in (("q", q), ("k", k), ("v", v), ("out", out)):
         if not t.is_cuda:
             raise GnaError(f"{name} must be a CUDA tensor (no CPU fallback)")
-        want = torch.float8_e4m3fn if (fp8 and name != "out") else torch.bfloat16
+        want = torch.float8_e4m3fn if (fp8 and name != "out") else t16
         if t.dtype != want:
-            raise GnaError(f"{name} must be {want} (q, k, v all bfloat16, or all float8_e4m3fn with a bfloat16 out)")
+            raise GnaError(f"{name} must be {want} (q, k, v, out all bfloat16 or all float16, or q, k, v "
+                           f"float8_e4m3fn with a bfloat16 out)")
         if not t.is_contiguous():
             raise GnaError(f"{name} must be contiguous")
     if lse is not None and (lse.dtype != torch.float32 or not lse.is_contiguous() or not lse.is_cuda):
@@ -167,8 +171,8 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
     n_extra = 0
     if extra_k is not None:
         for name, t in (("extra_k", extra_k), ("extra_v", extra_v)):
-            if t is None or not t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
-                raise GnaError(f"{name} must be a contiguous CUDA bfloat16 tensor [B, T, H, D]")
+            if t is None or not t.is_cuda or t.dtype != t16 or not t.is_contiguous():
+                raise GnaError(f"{name} must be a contiguous CUDA {t16} tensor [B, T, H, D]")
         if extra_k.shape != extra_v.shape or extra_k.dim() != 4 or extra_k.shape[0] != batch or \
                 tuple(extra_k.shape[2:]) != (heads, head_dim):
             raise GnaError("extra_k/extra_v must be [B, T, H, D] matching q")
@@ -180,14 +184,14 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
                      lse=(lse.data_ptr() if lse is not None else None), stream=stream, box=box,
                      work_range=work_range, flags=flags, workspace=ws_ptr, workspace_bytes=ws_bytes,
                      extra_k=ek, extra_v=ev, n_extra=n_extra,
-                     dtype=GNA_DTYPE_FP8_E4M3 if fp8 else GNA_DTYPE_BF16,
+                     dtype=GNA_DTYPE_FP8_E4M3 if fp8 else (GNA_DTYPE_FP16 if fp16 else GNA_DTYPE_BF16),
                      scales=tuple(scales) if scales is not None else (0.0, 0.0, 0.0))
 
 
 def forward(q, k, v, window, stride=None, dilation=None, causal=None, scale=None, out=None, lse=None,
             box=None, work_range=None, stream=None, return_lse=True, flags=0, workspace=None, extra_k=None,
             extra_v=None, scales=None):
-    """GNA forward on CUDA bf16 tensors [B, *spatial, H, D] (heads-last); optional extra
+    """GNA forward on CUDA bf16 (or fp16) tensors [B, *spatial, H, D] (heads-last); optional extra
     (text) keys/values [B, T, H, D] attended densely by every query.  q, k, v may instead be
     torch.float8_e4m3fn with per-tensor dequantisation scales=(q_scale, k_scale, v_scale)
     (GNA_DTYPE_FP8_E4M3, head_dim 128); out stays bfloat16.
@@ -196,7 +200,8 @@ def forward(q, k, v, window, stride=None, dilation=None, causal=None, scale=None
     import torch
 
     if out is None:
-        out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
+        out = torch.empty(q.shape, dtype=torch.float16 if q.dtype == torch.float16 else torch.bfloat16,
+                          device=q.device)
     if lse is None and return_lse:
         lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
     a = _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box, work_range, stream, flags,

@@ -1,12 +1,18 @@
 """GNA forward with E4M3 Q/K/V (GNA_DTYPE_FP8_E4M3)
 against the fp64 oracle run on the dequantised inputs.
 
-Tolerance (reading R17): the kernel's only rounding beyond the bf16 path is P -> E4M3
-before PV (RNE, 3 mantissa bits: relative error <= 2^-4 for P >= 2^-6, absolute <= 2^-10 below).
-With l >= 1 (the lazy running max never exceeds the row max), |dO| <= 2^-4 max|v| + n_small *
-2^-10 max|v| / l + bf16 output rounding; the rounding errors are unbiased, so their sum over the
-neighbourhood is far below the worst case.  Bound used: max-abs <= 2^-4 max|v| + 2e-2,
-mean-abs <= 2^-7 max|v| + 2e-3.  LSE depends only on fp32 row sums: 1e-3 as for bf16."""
+Tolerance (reading R17), per output element and scaled to the row's own data:
+the kernel's only rounding beyond the bf16 path is P -> E4M3 before PV (RNE, 3 mantissa
+bits): |dP| <= 2^-4 P for P >= 2^-6 (E4M3 normal range) and <= 2^-10 below.  Hence
+    |dO_d| <= 2^-4 * sum_k p_k |v_kd|  +  (subnormal P terms)  +  bf16 output rounding,
+with p_k = P_k / l the softmax weights.  A_d = sum_k p_k |v_kd| is exactly the oracle's
+forward on |v|, so the bound is computed per element:
+    max:  |O - O_ref| <= 2^-4 A + 2^-8 |O_ref| + 4e-3
+    mean: mean|O - O_ref| <= 2^-6 mean(A) + 1e-3
+(the 4e-3 / 1e-3 absolute terms cover the unbiased subnormal-P rounding, whose sum over
+a window grows like sqrt(#keys) x 2^-10).  On the discriminating inputs (|O| ~ 0.1-0.5)
+a PV-side error (wrong V box, P->V column mapping, scale) breaks the bound by >10x.
+LSE uses only fp32 row sums: 1e-3 as for bf16."""
 import numpy as np
 import pytest
 import torch
@@ -38,6 +44,18 @@ def _ids(c):
     return "x".join(map(str, c["spatial"])) + "_w" + "x".join(map(str, c["window"]))
 
 
+def _check_fp8(o, ro, ra, l, rl):
+    """o: kernel O, ro: oracle O on the dequantised inputs, ra: oracle forward on |v|."""
+    err = np.abs(o - ro)
+    bound = 2.0 ** -4 * ra + 2.0 ** -8 * np.abs(ro) + 4e-3
+    assert np.isfinite(o).all()
+    worst = float((err / bound).max())
+    assert worst <= 1.0, f"O error exceeds the per-element bound by {worst:.2f}x (max-abs {err.max():.3e})"
+    assert err.mean() <= 2.0 ** -6 * ra.mean() + 1e-3, f"O mean-abs {err.mean():.3e} vs mean A {ra.mean():.3e}"
+    assert np.abs(l - rl).max() <= 1e-3
+    return worst
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("disc", [False, True], ids=["normal", "discriminating"])
 @pytest.mark.parametrize("cfg", CFGS, ids=_ids)
@@ -51,13 +69,8 @@ def test_fp8_forward_vs_oracle(gna, cfg, disc):
     assert out.dtype == torch.bfloat16
     params = O.Params(cfg["spatial"], cfg["window"], cfg["stride"], cfg.get("dilation"), cfg.get("causal"))
     ro, rl = O.forward(qd.numpy(), kd.numpy(), vd.numpy(), params)
-    o = out.float().cpu().numpy()
-    err = np.abs(o - ro)
-    vmax = float(vd.abs().max())
-    assert np.isfinite(o).all()
-    assert err.max() <= 2.0 ** -4 * vmax + 2e-2, f"O max-abs {err.max()}"
-    assert err.mean() <= 2.0 ** -7 * vmax + 2e-3, f"O mean-abs {err.mean()}"
-    assert np.abs(lse.cpu().numpy() - rl).max() <= 1e-3
+    ra, _ = O.forward(qd.numpy(), kd.numpy(), np.abs(vd.numpy()), params)
+    _check_fp8(out.float().cpu().numpy(), ro, ra, lse.cpu().numpy(), rl)
 
 
 @pytest.mark.gpu
@@ -71,12 +84,13 @@ def test_fp8_rejects_unsupported(gna):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["c2b_flux64_s16", "c4a_hunyuan_blocked", "c3_cosmos"])
 def test_fp8_full_size_sampled(gna, name):
-    """E4M3 forward at BASELINE.json's full sizes (the launch bench.py --dtype fp8 times), sampled
-    rows incl. grid corners vs the oracle on the dequantised inputs; same tolerance as above."""
+    """E4M3 forward at BASELINE.json's full sizes (the launch bench.py --dtype fp8 times), on the
+    discriminating inputs, sampled rows incl. grid corners vs the oracle on the dequantised
+    inputs; same per-element tolerance as above."""
     from gna_inputs import WORKLOADS, sample_rows
     w = WORKLOADS[name]
     f = w.full()
-    q, k, v = make_qkv(w.batch, w.spatial, w.heads, w.head_dim, dtype=torch.float32)
+    q, k, v = make_qkv(w.batch, w.spatial, w.heads, w.head_dim, discriminating=True, dtype=torch.float32)
     (q8, qs, qd), (k8, ks, kd), (v8, vs, vd) = (quantize_e4m3(t) for t in (q, k, v))
     out, lse = gna.forward(q8.cuda(), k8.cuda(), v8.cuda(), f["window"], f["stride"], f["dilation"], f["causal"],
                            scales=(qs, ks, vs))
@@ -85,10 +99,7 @@ def test_fp8_full_size_sampled(gna, name):
     corners = [0, L[1] * L[2] - 1, w.n_tokens - 1, (L[0] // 2) * L[1] * L[2] + (L[1] // 2) * L[2] + L[2] // 2]
     rows = sample_rows(w.batch, w.spatial, w.heads, 64, extra_tokens=corners)
     ro, rl, _ = O.forward_rows(qd.numpy(), kd.numpy(), vd.numpy(), O.Params(**f), rows)
+    ra, _, _ = O.forward_rows(qd.numpy(), kd.numpy(), np.abs(vd.numpy()), O.Params(**f), rows)
     oo = out.float().cpu().reshape(w.batch, -1, w.heads, w.head_dim)[rows[:, 0], rows[:, 1], rows[:, 2]].numpy()
     ll = lse.cpu().reshape(w.batch, -1, w.heads)[rows[:, 0], rows[:, 1], rows[:, 2]].numpy()
-    err = np.abs(oo - ro)
-    vmax = float(vd.abs().max())
-    assert err.max() <= 2.0 ** -4 * vmax + 2e-2, f"O max-abs {err.max()}"
-    assert err.mean() <= 2.0 ** -7 * vmax + 2e-3, f"O mean-abs {err.mean()}"
-    assert np.abs(ll - rl).max() <= 1e-3
+    _check_fp8(oo, ro, ra, ll, rl)

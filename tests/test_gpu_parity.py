@@ -184,8 +184,10 @@ def test_direct_fused_permuted_paths_bitwise(gna, cfg):
     """Three routes to the same result, bit for bit: the default permute-free path
     (5-D TMA gathers + epilogue scatter), permute -> attention with the fused
     epilogue (GNA_FLAG_PERMUTED), and permute -> attention -> unpermute kernel
-    (GNA_FLAG_UNFUSED_EPILOGUE).  Masked / padded keys contribute exact zeros, so
-    the source of padding values (TMA zero fill vs permuted zero rows) is invisible."""
+    (GNA_FLAG_UNFUSED_EPILOGUE).  Masked and padded keys get P = 0 exactly (ex2 of
+    -inf on the MUFU and, since round 2, on the FMA-pipe polynomial too) and padded V rows
+    are zero on both routes (TMA zero fill / permuted zero rows), so they add exact zeros
+    and the two sources of padding are indistinguishable."""
     from paper_2504_16922_b200.gna import GNA_FLAG_PERMUTED, GNA_FLAG_UNFUSED_EPILOGUE
 
     for D in (128, 64, 32):

@@ -119,3 +119,31 @@ def test_sim_matches_multid_bruteforce(seed):
     pbs = bool((full[vis.astype(bool)] == 1).all())
     if all(l % t == 0 for l, t in zip(L, tk)):
         assert pbs == r["perfectly_block_sparse"]
+
+
+@pytest.mark.parametrize("L,T", [(10, 4), (13, 8), (5, 4)])
+def test_full_flags_padded_tile_never_full(L, T):
+    """Pins ora_full_bruteforce's padded-tile branch.  With window = extent every key is
+    attended by every query (self-attention limit), so the pair-by-pair check alone
+    would mark every visited tile full; a KV tile that runs past the extent holds padded
+    keys, which need predication, so it is NOT full.  L=10, T_KV=4: tiles [0,4)
+    and [4,8) are full, [8,12) is not."""
+    p = O.Params((L,), (L,), (1,))
+    vis = O.visits_bruteforce(p, (T,), (T,))
+    nk = -(-L // T)
+    assert vis.shape[1] == nk and (vis == 1).all()
+    full = O.full_bruteforce(p, (T,), (T,), vis)
+    expect = np.array([1] * (L // T) + [0] * (nk - L // T), dtype=np.uint8)
+    for row in full:
+        np.testing.assert_array_equal(row, expect)
+
+
+def test_full_flags_padded_tile_2d():
+    """2-D version: 10 x 8 dense with 4 x 4 tiles -> only the tiles of axis-0 block 2
+    (rows 8..11, past the extent 10) are not full."""
+    p = O.Params((10, 8), (10, 8), (1, 1))
+    vis = O.visits_bruteforce(p, (4, 4), (4, 4))
+    full = O.full_bruteforce(p, (4, 4), (4, 4), vis)
+    expect = np.array([1, 1, 1, 1, 0, 0], dtype=np.uint8)  # kv tiles (k0, k1) row-major, nk = (3, 2)
+    for row in full:
+        np.testing.assert_array_equal(row, expect)
