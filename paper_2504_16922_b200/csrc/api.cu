@@ -417,15 +417,16 @@ int plan_device_items(Plan& p, cudaStream_t st, int4** out) {
     int dev = 0;
     GNA_CUDA_TRY(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(p.mu);
-    int rc = plan_host_items(p);
-    if (rc) return rc;
     const bool capturing = stream_capturing(st);
     auto it = p.dev_items.find(dev);
     if (it == p.dev_items.end()) {
+        // checked before any allocation: an illegal call would invalidate the caller's capture
         if (capturing)
             return fail(GNA_EINVAL,
                         "first call for this problem on this device is inside a CUDA graph capture: "
-                        "call it once before capturing (the work list upload allocates device memory)");
+                        "call it once before capturing (the work list upload allocates memory)");
+        int rc = plan_host_items(p);
+        if (rc) return rc;
         DevItems d;
         GNA_CUDA_TRY(cudaMalloc(&d.ptr, p.host_count * sizeof(int4)));
         GNA_CUDA_TRY(cudaMemcpyAsync(d.ptr, p.host_items, p.host_count * sizeof(int4), cudaMemcpyHostToDevice, st));
