@@ -55,6 +55,9 @@
 #ifndef GNA_SPEC_EXP
 #define GNA_SPEC_EXP 0  // speculative exponentials of P chunk 0 with the running max: measured 20% slower (spills), A/B only
 #endif
+#ifndef GNA_LD_BATCH
+#define GNA_LD_BATCH 1  // the four S column loads issued back to back, one tcgen05.wait::ld (0: wait after each, A/B)
+#endif
 #ifndef GNA_V3_ELECT
 #define GNA_V3_ELECT 1
 #endif
@@ -475,12 +478,37 @@ __global__ void __launch_bounds__(384, 1)
             const int extra_left = p.n_extra - (j - nst_gna) * 128;
             const bool warp_full =
                 extra_stage ? extra_left >= 128 : __all_sync(0xffffffffu, row_full || !valid);
+            // 128-bit row mask of the stage (1 or 2 boxes), built from the row's coordinates
+            // BEFORE S is loaded, so the mask arithmetic is not live next to the 128 S registers
+            uint32_t mw[4] = {~0u, ~0u, ~0u, ~0u};
+            if (!warp_full) {
+                u128 m;
+                if (extra_stage) {
+                    m = bits_below(extra_left);  // keys [0, n_extra - e*128) of the extra stage
+                } else {
+                    m = box_row_mask(g, mconst, rlo[0], rhi[0]);
+                    if (KPB == 2) m |= box_row_mask(g, mconst, rlo[KPB - 1], rhi[KPB - 1]) << 64;
+                }
+                mw[0] = static_cast<uint32_t>(m);
+                mw[1] = static_cast<uint32_t>(m >> 32);
+                mw[2] = static_cast<uint32_t>(m >> 64);
+                mw[3] = static_cast<uint32_t>(m >> 96);
+            }
 
             ptx::mbar_wait(bar_s, j & 1);
             if (r == 0) GT(j, 4 * i + 0);
             if (r == 0 && i == 0 && j == 0) GTL(2);
             ptx::tc_fence_after();
             float s[128];
+#if GNA_LD_BATCH
+            // all four 32-column loads in flight at once, one wait (the register fences pin every
+            // use of s after the wait)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ptx::tmem_ld32f(tS + c * 32, &s[c * 32]);
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ptx::reg_fence32(&s[c * 32]);
+#else
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 uint32_t rr[32];
@@ -489,18 +517,10 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
             }
+#endif
             if (r == 0) GT(j, 4 * i + 1);
             if (!warp_full) {
-                // 128-bit row mask of the stage (1 or 2 boxes), then one select per element
-                u128 m;
-                if (extra_stage) {
-                    m = bits_below(extra_left);  // keys [0, n_extra - e*128) of the extra stage
-                } else {
-                    m = box_row_mask(g, mconst, rlo[0], rhi[0]);
-                    if (KPB == 2) m |= box_row_mask(g, mconst, rlo[KPB - 1], rhi[KPB - 1]) << 64;
-                }
-                const uint32_t mw[4] = {static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32),
-                                        static_cast<uint32_t>(m >> 64), static_cast<uint32_t>(m >> 96)};
+                // one select per element
 #pragma unroll
                 for (int c = 0; c < 128; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
             }

@@ -102,15 +102,19 @@ __global__ void __launch_bounds__(256) unpermute_kernel(Geometry g, const uint4*
         const BoxUnit u = decode_unit(g, unit);
         uint4 val[NP];
         float lv[NP];
+        long long nrs[NP];
+        // padding rows of the permuted O are never written by the attention kernel: they are
+        // neither read nor stored (crop)
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const long long pr = u.perm_row0 + r0 + p * RPP;
-            val[p] = __ldg(op + pr * VPR + vcol);
-            lv[p] = vcol == 0 ? __ldg(lsep + pr) : 0.f;
+            nrs[p] = nat_row(g, u, r0 + p * RPP);
+            val[p] = nrs[p] >= 0 ? __ldg(op + pr * VPR + vcol) : make_uint4(0, 0, 0, 0);
+            lv[p] = (vcol == 0 && nrs[p] >= 0) ? __ldg(lsep + pr) : 0.f;
         }
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            const long long nr = nat_row(g, u, r0 + p * RPP);
+            const long long nr = nrs[p];
             if (nr < 0) continue;
             if (vcol < vout) out[nr * vout + vcol] = val[p];
             if (vcol == 0 && lse != nullptr) lse[nr] = lv[p];
