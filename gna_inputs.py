@@ -63,6 +63,8 @@ WORKLOADS = {w.name: w for w in [
              note="paper headline (Fig.4, P:383-384), perfectly block-sparse"),
     Workload("x2_flux4k", (256, 256), (80, 80), (16, 16), heads=24,
              note="paper FLUX 4K shape (P:986-989)"),
+    Workload("x3_cosmos89", (16, 44, 80), (16, 24, 16), (1, 8, 16), heads=32,
+             note="paper Cosmos-7B 89% sparsity shape (Fig.5 P:519, Tab.2 P:674-717), perfectly block-sparse"),
     Workload("s1_sweep1d", (8192,), (1024,), (1,), dilation=(2,), causal=(True,), batch=8, heads=16,
              note="configs[4] sweep 1-D, dilation 2, causal"),
     Workload("s2_sweep2d", (128, 128), (32, 32), (8, 8), dilation=(2, 2), batch=8, heads=16,

@@ -98,9 +98,9 @@ extern "C" {
  * stored value x scale), bf16 O and fp32 LSE -- the FP8 forward the paper quotes for its
  * Blackwell kernel.  QK^T and PV run as E4M3
  * tcgen05 MMAs (kind::f8f6f4, fp32 accumulation); P is rounded to E4M3 (RNE, saturating)
- * before PV, the softmax and row sums stay fp32.  head_dim 128, no extra KV tokens, and
- * only the permute-free path (gna_forward / gna_forward_ex); the stage API returns
- * GNA_EUNSUPPORTED for it. */
+ * before PV, the softmax and row sums stay fp32.  head_dim 128 and only the permute-free
+ * path (gna_forward / gna_forward_ex); the stage API returns GNA_EUNSUPPORTED for it.
+ * Extra KV tokens are E4M3 too and share k_scale / v_scale with k / v. */
 #define GNA_DTYPE_FP8_E4M3 2
 
 /* flags */
@@ -135,9 +135,9 @@ typedef struct gna_args {
     int flags;
     /* Extra (text) KV tokens fused into the same kernel:
      * n_extra keys/values per (batch, head), layout [B][n_extra][H][D] in q's
-     * 16-bit dtype (bf16 or fp16), attended densely by EVERY query in the same
-     * softmax as its GNA neighbourhood.  0 / NULL = none.  Requires
-     * head_dim >= 64. */
+     * dtype (bf16, fp16, or E4M3 sharing k_scale / v_scale), attended densely
+     * by EVERY query in the same softmax as its GNA neighbourhood.  0 / NULL =
+     * none.  Requires head_dim >= 64. */
     const void *extra_k, *extra_v;
     int n_extra;
     /* GNA_DTYPE_FP8_E4M3 only: per-tensor dequantisation scales (<= 0 -> 1). */

@@ -65,7 +65,6 @@ int validate(const gna_args* a, bool need_ptrs) {
         return fail(GNA_EUNSUPPORTED, "dtype: GNA_DTYPE_BF16, GNA_DTYPE_FP16 or GNA_DTYPE_FP8_E4M3");
     if (a->dtype == GNA_DTYPE_FP8_E4M3) {
         if (a->head_dim != 128) return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 needs head_dim 128");
-        if (a->n_extra > 0) return fail(GNA_EUNSUPPORTED, "GNA_DTYPE_FP8_E4M3 with extra KV tokens is not supported");
         if (!(a->q_scale >= 0.f && a->k_scale >= 0.f && a->v_scale >= 0.f))
             return fail(GNA_EINVAL, "q_scale/k_scale/v_scale must be >= 0 (0 = 1)");
     }
@@ -227,6 +226,16 @@ Built build_items(const Geometry& g) {
             i += 1;
         }
     }
+    // Every planned sub-tile has an in-bounds query and every query attends at least itself, so
+    // no item has an empty KV range (the kernel's roles rely on >= 1 stage per item); the
+    // filter below is a guard that never removes anything.
+    out.items.erase(std::remove_if(out.items.begin(), out.items.end(),
+                                   [&](const int4& it) {
+                                       int lo[3], hi[3];
+                                       sub_range(g, it.x, it.y, lo, hi);
+                                       return (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]) <= 0;
+                                   }),
+                    out.items.end());
     for (auto& it : out.items) {
         int lo[3], hi[3];
         sub_range(g, it.x, it.y, lo, hi);
@@ -589,7 +598,10 @@ int make_tmap_extra(CUtensorMap* m, const void* base, const Geometry& g, int n_e
     const cuuint64_t D = g.D, H = g.heads;
     cuuint64_t dims[3] = {D, H, static_cast<cuuint64_t>(g.batch) * n_extra};
     cuuint64_t strides[2] = {D * 2, H * D * 2};
-    cuuint32_t box[3] = {64, 1, 128};
+    const cuuint64_t E = dt == CU_TENSOR_MAP_DATA_TYPE_UINT8 ? 1 : 2;
+    strides[0] = D * E;
+    strides[1] = H * D * E;
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(128 / E), 1, 128};  // one 128-byte swizzle row
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = enc(m, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -682,8 +694,9 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     memset(&tev, 0, sizeof tev);
     if (a->n_extra > 0) {
         if (!a->extra_k || !a->extra_v) return fail(GNA_EINVAL, "extra_k/extra_v NULL with n_extra > 0");
-        if ((rc = make_tmap_extra(&tek, a->extra_k, c.g, a->n_extra, dt16))) return rc;
-        if ((rc = make_tmap_extra(&tev, a->extra_v, c.g, a->n_extra, dt16))) return rc;
+        const CUtensorMapDataType dte = a->dtype == GNA_DTYPE_FP8_E4M3 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : dt16;
+        if ((rc = make_tmap_extra(&tek, a->extra_k, c.g, a->n_extra, dte))) return rc;
+        if ((rc = make_tmap_extra(&tev, a->extra_v, c.g, a->n_extra, dte))) return rc;
     }
     AttnParams p{};
     p.direct = direct ? 1 : 0;

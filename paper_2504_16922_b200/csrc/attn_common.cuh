@@ -54,7 +54,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define GNA_POLY_EVERY 8  // 1 exp pair in GNA_POLY_EVERY on the FMA pipe (0 = all MUFU)
 #endif
 #ifndef GNA_NS128
-#define GNA_NS128 4  // K/V ring slots of 32 KB at head_dim 128
+#define GNA_NS128 3  // K/V ring slots of 32 KB at head_dim 128 (next to the double-buffered Q)
 #endif
 #ifndef GNA_PSPLIT
 #define GNA_PSPLIT 2  // P is handed to the MMA in GNA_PSPLIT chunks (1, 2 or 4): the PV of the
@@ -71,13 +71,16 @@ struct Cfg {
     static constexpr int ONH = DP / 64;              // 128-byte chunks of a bf16 O row
     static constexpr int CHUNK_BYTES = 128 * 128;    // 128 rows x 128 B, one SW128 chunk
     static constexpr int TILE_BYTES = NH * CHUNK_BYTES;  // 128 rows x DP elements
-    static constexpr int NS = F8 ? 8 : (DP == 128 ? GNA_NS128 : 8);  // KV ring slots (K and V share it)
+    static constexpr int NS = F8 ? 6 : (DP == 128 ? GNA_NS128 : 8);  // KV ring slots (K and V share it)
     static constexpr int KPB = 128 / BV;             // boxes per 128-row tile
     static constexpr int KSTEP = F8 ? 32 : 16;       // MMA K per instruction
-    static constexpr int Q_OFF = 0;
-    static constexpr int KV_OFF = 2 * TILE_BYTES;
-    static constexpr int BAR_OFF = KV_OFF + NS * TILE_BYTES;
+    static constexpr int Q_OFF = 0;                  // 2 buffers x 2 sub-tiles (the next item's Q loads early)
+    static constexpr int KV_OFF = 4 * TILE_BYTES;
+    static constexpr int OST_OFF = KV_OFF + NS * TILE_BYTES;       // E4M3 only: bf16 O staging, 2 sub-tiles
+    static constexpr int OST_BYTES = F8 ? 2 * 2 * CHUNK_BYTES : 0;
+    static constexpr int BAR_OFF = OST_OFF + OST_BYTES;
     static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
+    static_assert(SMEM_BYTES <= 232448, "shared memory budget (227 KB per CTA)");
     static constexpr int THREADS = 384;
 };
 
@@ -102,6 +105,50 @@ __device__ __forceinline__ void decode_stage(const Geometry& g, const int lo[3],
         sb.lin[u] = ((lo[0] + k0) * g.nb[1] + (lo[1] + k1)) * g.nb[2] + (lo[2] + k2);
     }
 }
+
+// Class-local coordinates of row r (TMEM lane) of Q sub-tile `sub`: the sub-tile is QB boxes
+// per axis, box u in row-major order, rows of a box row-major (i0, i1, i2).
+__device__ __forceinline__ void row_coords(const Geometry& g, int sub, int r, int x[3]) {
+    int sc[3];
+    sub_coords(g, sub, sc);
+    const int BV = g.box_vol;
+    const int ub = r / BV, inner = r % BV;
+    const int u2 = ub % g.QB[2], u1 = (ub / g.QB[2]) % g.QB[1], u0 = ub / (g.QB[2] * g.QB[1]);
+    x[2] = (sc[2] * g.QB[2] + u2) * g.B[2] + (inner & (g.B[2] - 1));
+    x[1] = (sc[1] * g.QB[1] + u1) * g.B[1] + ((inner >> g.logB[2]) & (g.B[1] - 1));
+    x[0] = (sc[0] * g.QB[0] + u0) * g.B[0] + (inner >> (g.logB[2] + g.logB[1]));
+}
+
+// Incremental walk over an item's union KV box range [lo, lo + ext) in row-major order
+// (the order decode_stage defines), KPB boxes per stage: no integer division per stage.
+struct BoxCursor {
+    int k[3];   // class-local box coordinates of the next box
+    int idx;    // linear index of the next box inside the range
+    __device__ __forceinline__ void init(const int lo[3]) {
+        k[0] = lo[0];
+        k[1] = lo[1];
+        k[2] = lo[2];
+        idx = 0;
+    }
+    // the stage's boxes (filler boxes past nkv are marked dead and point at lo), then advance
+    __device__ __forceinline__ void stage(const int lo[3], const int ext[3], int nkv, int kpb, StageBoxes& sb) {
+        for (int u = 0; u < kpb; ++u) {
+            const bool dead = idx >= nkv;
+            sb.dead[u] = dead;
+            sb.k[u][0] = dead ? lo[0] : k[0];
+            sb.k[u][1] = dead ? lo[1] : k[1];
+            sb.k[u][2] = dead ? lo[2] : k[2];
+            ++idx;
+            if (++k[2] == lo[2] + ext[2]) {
+                k[2] = lo[2];
+                if (++k[1] == lo[1] + ext[1]) {
+                    k[1] = lo[1];
+                    ++k[0];
+                }
+            }
+        }
+    }
+};
 
 // ---- separable GNA mask of one row over one box, as a bit mask over the
 // box's rows (row-major (i0, i1, i2)).  Axis intervals [lo, hi) are relative

@@ -171,8 +171,9 @@ def _tensor_args(q, k, v, out, lse, window, stride, dilation, causal, scale, box
     n_extra = 0
     if extra_k is not None:
         for name, t in (("extra_k", extra_k), ("extra_v", extra_v)):
-            if t is None or not t.is_cuda or t.dtype != t16 or not t.is_contiguous():
-                raise GnaError(f"{name} must be a contiguous CUDA {t16} tensor [B, T, H, D]")
+            want = torch.float8_e4m3fn if fp8 else t16
+            if t is None or not t.is_cuda or t.dtype != want or not t.is_contiguous():
+                raise GnaError(f"{name} must be a contiguous CUDA {want} tensor [B, T, H, D]")
         if extra_k.shape != extra_v.shape or extra_k.dim() != 4 or extra_k.shape[0] != batch or \
                 tuple(extra_k.shape[2:]) != (heads, head_dim):
             raise GnaError("extra_k/extra_v must be [B, T, H, D] matching q")

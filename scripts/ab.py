@@ -1,4 +1,5 @@
-"""Build compile-time variants of the library and benchmark them back to back.
+"""Build compile-time variants of the library and benchmark them back to back
+(per run: TFLOP/s, median SM MHz under load, TFLOP/s per GHz).
 
 usage (here):    python scripts/ab.py build NAME=-DFLAG=1,-DOTHER=2 ...
        (GPU box) python scripts/ab.py run WORKLOAD[,WORKLOAD] NAME ...
@@ -23,7 +24,7 @@ def build(specs):
 
 def run(workloads, names):
     res = {}
-    for rep in range(2):
+    for rep in range(int(os.environ.get("AB_REPS", "2"))):
         for name in names:
             lname, _, envspec = name.partition("@")  # NAME@VAR=VAL[,VAR=VAL]: extra environment
             lib = os.path.join(VDIR, f"libgna_{lname}.so") if lname != "base" else os.path.join(
@@ -35,12 +36,12 @@ def run(workloads, names):
                     env[k] = v
                 extra = os.environ.get("AB_ARGS", "").split()
                 out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", wl, "--steps", "10",
-                                      "--warmup", "3", "--no-cpu-baseline", *extra], env=env, capture_output=True,
+                                      "--warmup", "3", "--no-cpu-baseline", "--no-verify", *extra], env=env, capture_output=True,
                                      text=True, timeout=600)
                 try:
                     d = json.loads(out.stdout.strip().splitlines()[-1])
-                    res.setdefault((name, wl), []).append((d["value"], d.get("permuted_pipeline_attention_tflops") or 0.0,
-                                                           d["clocks"]["sm_mhz"]))
+                    mhz = d["clocks"]["sm_mhz"] or 0.0
+                    res.setdefault((name, wl), []).append((d["value"], mhz, d["value"] / mhz * 1000.0 if mhz else 0.0))
                 except Exception:
                     res.setdefault((name, wl), []).append(("ERR", out.stderr[-300:]))
     for (name, wl), v in sorted(res.items(), key=lambda x: (x[0][1], x[0][0])):

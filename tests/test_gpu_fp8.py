@@ -103,3 +103,33 @@ def test_fp8_full_size_sampled(gna, name):
     oo = out.float().cpu().reshape(w.batch, -1, w.heads, w.head_dim)[rows[:, 0], rows[:, 1], rows[:, 2]].numpy()
     ll = lse.cpu().reshape(w.batch, -1, w.heads)[rows[:, 0], rows[:, 1], rows[:, 2]].numpy()
     _check_fp8(oo, ro, ra, ll, rl)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T", [77, 200])
+def test_fp8_extra_kv(gna, T):
+    """E4M3 with extra (text) KV tokens (NEXT-1 x NEXT-3): the extra K/V are E4M3 with the same
+    per-tensor scales as K/V (amax over the GNA and extra tokens together)."""
+    cfg = CFGS[3]
+    B, H, D = 2, 2, 128
+    q, k, v = make_qkv(B, cfg["spatial"], H, D, discriminating=True, dtype=torch.float32)
+    g = torch.Generator("cpu").manual_seed(91)
+    ek = torch.randn((B, T, H, D), generator=g)
+    ev = torch.rand((B, T, H, D), generator=g) * 2 - 1
+
+    def quant_pair(a, b):
+        scale = float(max(a.abs().max(), b.abs().max())) / 448.0
+        qa, qb = (a / scale).to(torch.float8_e4m3fn), (b / scale).to(torch.float8_e4m3fn)
+        return qa, qb, scale, qa.float() * scale, qb.float() * scale
+
+    q8, qs, qd = quantize_e4m3(q)
+    k8, ek8, ks, kd, ekd = quant_pair(k, ek)
+    v8, ev8, vs, vd, evd = quant_pair(v, ev)
+    out, lse = gna.forward(q8.cuda(), k8.cuda(), v8.cuda(), cfg["window"], cfg["stride"], cfg.get("dilation"),
+                           cfg.get("causal"), scales=(qs, ks, vs), extra_k=ek8.cuda(), extra_v=ev8.cuda())
+    torch.cuda.synchronize()
+    params = O.Params(cfg["spatial"], cfg["window"], cfg["stride"], cfg.get("dilation"), cfg.get("causal"))
+    ro, rl = O.forward(qd.numpy(), kd.numpy(), vd.numpy(), params, extra_k=ekd.numpy(), extra_v=evd.numpy())
+    ra, _ = O.forward(qd.numpy(), kd.numpy(), np.abs(vd.numpy()), params, extra_k=ekd.numpy(),
+                      extra_v=np.abs(evd.numpy()))
+    _check_fp8(out.float().cpu().numpy(), ro, ra, lse.cpu().numpy(), rl)
