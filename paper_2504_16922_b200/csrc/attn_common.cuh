@@ -36,7 +36,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
     do {                                                                               \
         if ((w) < GNA_TL_CTAS) g_gna_tl[(w)][(ev)] = gtimer();                         \
     } while (0)
+// per work item of the launch (persistent kernel): g_gna_ti[t][ev], t = item index in the range
+static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
+#define GTI(t, ev)                                                                     \
+    do {                                                                               \
+        if ((t) < GNA_TL_CTAS) g_gna_ti[(t)][(ev)] = gtimer();                         \
+    } while (0)
 #else
+#define GTI(t, ev) \
+    do {           \
+    } while (0)
 #define GTL(ev) \
     do {        \
     } while (0)
@@ -53,8 +62,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #ifndef GNA_POLY_EVERY
 #define GNA_POLY_EVERY 8  // 1 exp pair in GNA_POLY_EVERY on the FMA pipe (0 = all MUFU)
 #endif
+#ifndef GNA_QBUF
+#define GNA_QBUF 1  // Q buffers (2: the next item's Q loads while the current item runs)
+#endif
 #ifndef GNA_NS128
-#define GNA_NS128 3  // K/V ring slots of 32 KB at head_dim 128 (next to the double-buffered Q)
+#define GNA_NS128 (GNA_QBUF == 2 ? 3 : 4)  // K/V ring slots of 32 KB at head_dim 128
 #endif
 #ifndef GNA_PSPLIT
 #define GNA_PSPLIT 2  // P is handed to the MMA in GNA_PSPLIT chunks (1, 2 or 4): the PV of the
@@ -74,8 +86,9 @@ struct Cfg {
     static constexpr int NS = F8 ? 6 : (DP == 128 ? GNA_NS128 : 8);  // KV ring slots (K and V share it)
     static constexpr int KPB = 128 / BV;             // boxes per 128-row tile
     static constexpr int KSTEP = F8 ? 32 : 16;       // MMA K per instruction
-    static constexpr int Q_OFF = 0;                  // 2 buffers x 2 sub-tiles (the next item's Q loads early)
-    static constexpr int KV_OFF = 4 * TILE_BYTES;
+    static constexpr int QBUF = GNA_QBUF;
+    static constexpr int Q_OFF = 0;                  // QBUF buffers x 2 sub-tiles
+    static constexpr int KV_OFF = 2 * QBUF * TILE_BYTES;
     static constexpr int OST_OFF = KV_OFF + NS * TILE_BYTES;       // E4M3 only: bf16 O staging, 2 sub-tiles
     static constexpr int OST_BYTES = F8 ? 2 * 2 * CHUNK_BYTES : 0;
     static constexpr int BAR_OFF = OST_OFF + OST_BYTES;

@@ -220,11 +220,19 @@ __global__ void __launch_bounds__(384, 1)
                         const int4 item = __ldg(p.items + widx);
                         const int4 cc4 = __ldg(p.item_info + 3 * widx + 2);
                         const int ccl[3] = {cc4.x, cc4.y, cc4.z};
-                        const int b = kq & 1;
-                        if (kq >= 2) ptx::mbar_wait(bar_qfree(b), ((kq >> 1) - 1) & 1);
+                        const int b = kq % C::QBUF;
+                        if (kq >= C::QBUF) ptx::mbar_wait(bar_qfree(b), ((kq / C::QBUF) - 1) & 1);
                         const bool hasB = item.z >= 0;
                         ptx::mbar_expect_tx(bar_q(b), (hasB ? 2 : 1) * C::TILE_BYTES);
                         if (kq == 0) GTL(13);
+                        GTI(t, 0);
+#ifdef GNA_TRACE
+                        {
+                            unsigned smid;
+                            asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+                            if (t < GNA_TL_CTAS) g_gna_ti[t][7] = smid;
+                        }
+#endif
                         for (int i = 0; i < (hasB ? 2 : 1); ++i) {
                             int sc[3];
                             sub_coords(g, i == 0 ? item.y : item.z, sc);
@@ -264,6 +272,7 @@ __global__ void __launch_bounds__(384, 1)
                                 ptx::mbar_wait(bar_kv_empty(slot), ph ^ 1u);
                                 GT(j, 12 + kind);
                                 if (first_load) GTL(1);
+                                if (j == 0 && kind == 0) GTI(t, 1);
                                 first_load = false;
                                 ptx::mbar_expect_tx(bar_kv_full(slot), C::TILE_BYTES);
                                 if (j < nst_gna) {
@@ -367,10 +376,11 @@ __global__ void __launch_bounds__(384, 1)
                     const int nkv = __ldg(p.item_info + 3 * widx).w;
                     const int nst = (nkv + KPB - 1) / KPB + p.extra_stages;
                     const bool hasB = item.z >= 0;
-                    const int b = kq & 1;
+                    const int b = kq % C::QBUF;
                     const uint32_t q16a = (2 * b) * TILE16, q16b = q16a + TILE16;
-                    ptx::mbar_wait(bar_q(b), (kq >> 1) & 1);
+                    ptx::mbar_wait(bar_q(b), (kq / C::QBUF) & 1);
                     if (lane == 0 && kq == 0) GTL(11);
+                    if (lane == 0) GTI(t, 6);
                     int slotK, slotV;
                     take(slotK);
                     ptx::tc_fence_after();
@@ -444,7 +454,7 @@ __global__ void __launch_bounds__(384, 1)
             long long bh, widx;
             decode_w(p.work_begin + t, bh, widx);
             const int4 item = __ldg(p.items + widx);
-            const int b = kq & 1;
+            const int b = kq % C::QBUF;
             const int sub = i == 0 ? item.y : item.z;
             if (sub < 0) {  // no sub-tile B in this item: nothing to compute, Q buffer b not used by WG 1
                 if (r == 0) ptx::mbar_arrive(bar_qfree(b));
@@ -537,6 +547,7 @@ __global__ void __launch_bounds__(384, 1)
                 ptx::mbar_wait(bar_s, sph & 1);
                 if (r == 0) GT(j, 4 * i + 0);
                 if (r == 0 && i == 0 && j == 0) GTL(2);
+                if (r == 0 && j == 0) GTI(t, i == 0 ? 2 : 8);
                 ptx::tc_fence_after();
                 float s[128];
 #if GNA_LD_BATCH
@@ -657,6 +668,7 @@ __global__ void __launch_bounds__(384, 1)
                 ptx::mbar_arrive(bar_p);
             }
             if (r == 0 && i == 0) GTL(3);
+            if (r == 0 && i == 0) GTI(t, 3);
 
             // ---------------------------------------------------------- epilogue
             // the row's position, recomputed from the (laundered) work index
@@ -779,6 +791,7 @@ __global__ void __launch_bounds__(384, 1)
                 *lrow = (m_eff + __log2f(l_run)) * 0.69314718055994530942f;
             }
             if (r == 0 && i == 0) GTL(4);
+            if (r == 0) GTI(t, 4 + i);
             ++ni;
         }
         ptx::tc_fence_before();
@@ -859,10 +872,15 @@ extern "C" int gna_debug_timeline(void* host, size_t bytes) {
     if (bytes > sizeof(g_gna_tl)) bytes = sizeof(g_gna_tl);
     return cudaMemcpyFromSymbol(host, g_gna_tl, bytes) == cudaSuccess ? 0 : 3;
 }
+extern "C" int gna_debug_items(void* host, size_t bytes) {
+    if (bytes > sizeof(g_gna_ti)) bytes = sizeof(g_gna_ti);
+    return cudaMemcpyFromSymbol(host, g_gna_ti, bytes) == cudaSuccess ? 0 : 3;
+}
 extern "C" int gna_debug_trace_reset(void) {
     static unsigned long long zeros[GNA_TRACE_CTAS * GNA_TRACE_STAGES * 16];
     static unsigned long long zeros_tl[GNA_TL_CTAS * 16];
     if (cudaMemcpyToSymbol(g_gna_tl, zeros_tl, sizeof(zeros_tl)) != cudaSuccess) return 3;
+    if (cudaMemcpyToSymbol(g_gna_ti, zeros_tl, sizeof(zeros_tl)) != cudaSuccess) return 3;
     return cudaMemcpyToSymbol(g_gna_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 3;
 }
 #endif
