@@ -456,10 +456,10 @@ __global__ void __launch_bounds__(384, 1)
             const int4 item = __ldg(p.items + widx);
             const int b = kq % C::QBUF;
             const int sub = i == 0 ? item.y : item.z;
-            if (sub < 0) {  // no sub-tile B in this item: nothing to compute, Q buffer b not used by WG 1
-                if (r == 0) ptx::mbar_arrive(bar_qfree(b));
-                continue;
-            }
+            // no sub-tile B in this item: nothing to compute.  WG 0 releases the Q buffer for both
+            // (arrival count 2): an early arrival from here could complete the phase of an item
+            // WG 0 is still working on when two B-less items follow each other
+            if (sub < 0) continue;
             const int4* info = p.item_info + 3 * widx;
             const int nkv = __ldg(info).w;
             const int nst_gna = (nkv + KPB - 1) / KPB;
@@ -768,11 +768,11 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     ptx::bulk_commit();
                     ptx::bulk_wait_read0();  // smem read by the TMA: the Q buffer may be refilled
-                    ptx::mbar_arrive(bar_qfree(b));
+                    ptx::mbar_arrive_cnt(bar_qfree(b), item_e.z >= 0 ? 1u : 2u);
                 }
                 if (F8) asm volatile("bar.sync %0, 128;" ::"r"(1 + i) : "memory");  // staging area reused next item
             } else {
-                if (r == 0) ptx::mbar_arrive(bar_qfree(b));
+                if (r == 0) ptx::mbar_arrive_cnt(bar_qfree(b), item_e.z >= 0 ? 1u : 2u);
                 if (valid) {
 #pragma unroll
                     for (int c = 0; c < DP / 32; ++c) {
