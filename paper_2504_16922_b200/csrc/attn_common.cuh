@@ -65,8 +65,22 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
 #ifndef GNA_QBUF
 #define GNA_QBUF 1  // Q buffers (2: the next item's Q loads while the current item runs)
 #endif
+#ifndef GNA_EARLY_Q
+#define GNA_EARLY_Q 0  // 1: the MMA warp frees the Q buffer once the item's last QK^T completes (O is
+                       // staged for its TMA store in a dedicated buffer), so the next item's Q loads
+                       // while the current item's last stage and epilogue run
+#endif
+#ifndef GNA_QWAIT_NS
+#define GNA_QWAIT_NS 256  // sleep between polls of the Q producer's "Q buffer free" wait
+#endif
+#ifndef GNA_KVWAIT_NS
+#define GNA_KVWAIT_NS 64  // sleep between polls of the K/V producer's "ring slot free" wait
+#endif
 #ifndef GNA_NS128
 #define GNA_NS128 (GNA_QBUF == 2 ? 3 : 4)  // K/V ring slots of 32 KB at head_dim 128
+#endif
+#ifndef GNA_EXP_LAG
+#define GNA_EXP_LAG 0  // softmax exp loop software-pipelined by this many key pairs (0: sum/pack right behind)
 #endif
 #ifndef GNA_PSPLIT
 #define GNA_PSPLIT 2  // P is handed to the MMA in GNA_PSPLIT chunks (1, 2 or 4): the PV of the
@@ -89,8 +103,12 @@ struct Cfg {
     static constexpr int QBUF = GNA_QBUF;
     static constexpr int Q_OFF = 0;                  // QBUF buffers x 2 sub-tiles
     static constexpr int KV_OFF = 2 * QBUF * TILE_BYTES;
-    static constexpr int OST_OFF = KV_OFF + NS * TILE_BYTES;       // E4M3 only: bf16 O staging, 2 sub-tiles
-    static constexpr int OST_BYTES = F8 ? 2 * 2 * CHUNK_BYTES : 0;
+    static constexpr bool EARLY_Q = GNA_EARLY_Q != 0;
+    static_assert(!EARLY_Q || QBUF == 1, "early Q release: one Q buffer (the O staging buffer takes the room)");
+    // O staging for the TMA-store epilogue: E4M3 one bf16 O tile per sub-tile; 16-bit types with
+    // EARLY_Q one O tile shared by the two sub-tiles (used in turn); otherwise O is staged in the Q buffer
+    static constexpr int OST_OFF = KV_OFF + NS * TILE_BYTES;
+    static constexpr int OST_BYTES = F8 ? 2 * 2 * CHUNK_BYTES : (EARLY_Q ? ONH * CHUNK_BYTES : 0);
     static constexpr int BAR_OFF = OST_OFF + OST_BYTES;
     static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
     static_assert(SMEM_BYTES <= 232448, "shared memory budget (227 KB per CTA)");

@@ -144,6 +144,9 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t bar_o_free0 = bar_o_full0 + 16;          // [2] O_i drained from TMEM (128)
     const uint32_t bar_pc0 = bar_o_free0 + 16;              // [2][3] P chunk c of sub-tile i ready
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sgen + C::BAR_OFF + 32 + 16 * C::NS + 64 + 48);
+    // shared O staging buffer released by its TMA store (16-bit types, EARLY_Q): one phase per use,
+    // uses in item order, sub-tile A before B
+    const uint32_t bar_ost = bar0 + 32u + 16u * C::NS + 64u + 48u + 8u;
 
     if (threadIdx.x == 0) {
         GT(0, 15);
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(384, 1)
 #endif
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(bar_q(b), 1);
-            ptx::mbar_init(bar_qfree(b), 2);
+            ptx::mbar_init(bar_qfree(b), C::EARLY_Q ? 1 : 2);
         }
         for (int s = 0; s < C::NS; ++s) {
             ptx::mbar_init(bar_kv_full(s), 1);
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(384, 1)
             ptx::mbar_init(bar_o_free0 + 8 * i, 128);
         }
         for (int c = 0; c < 6; ++c) ptx::mbar_init(bar_pc0 + 8 * c, 128);
+        ptx::mbar_init(bar_ost, 1);
         ptx::fence_mbar_init();
     }
     if (warp == 8) {
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(384, 1)
                         const int4 cc4 = __ldg(p.item_info + 3 * widx + 2);
                         const int ccl[3] = {cc4.x, cc4.y, cc4.z};
                         const int b = kq % C::QBUF;
-                        if (kq >= C::QBUF) ptx::mbar_wait(bar_qfree(b), ((kq / C::QBUF) - 1) & 1);
+                        if (kq >= C::QBUF) ptx::mbar_wait_sleep(bar_qfree(b), ((kq / C::QBUF) - 1) & 1, GNA_QWAIT_NS);
                         const bool hasB = item.z >= 0;
                         ptx::mbar_expect_tx(bar_q(b), (hasB ? 2 : 1) * C::TILE_BYTES);
                         if (kq == 0) GTL(13);
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(384, 1)
                         for (int j = 0; j < nst; ++j) {
                             if (j < nst_gna) cur.stage(lo, ext, nkv, KPB, sb);
                             for (int kind = 0; kind < 2; ++kind) {
-                                ptx::mbar_wait(bar_kv_empty(slot), ph ^ 1u);
+                                ptx::mbar_wait_sleep(bar_kv_empty(slot), ph ^ 1u, GNA_KVWAIT_NS);
                                 GT(j, 12 + kind);
                                 if (first_load) GTL(1);
                                 if (j == 0 && kind == 0) GTI(t, 1);
@@ -392,6 +396,7 @@ __global__ void __launch_bounds__(384, 1)
                         GNA_COMMIT(bar_s_full0 + 8);
                     }
                     GNA_COMMIT(bar_kv_empty(slotK));
+                    if (C::EARLY_Q && nst == 1) GNA_COMMIT(bar_qfree(b));  // the item's last QK^T issued
                     for (int j = 0; j < nst; ++j) {
                         take(slotV);
                         if (lane == 0) GT(j, 8);
@@ -428,6 +433,8 @@ __global__ void __launch_bounds__(384, 1)
                                 GNA_COMMIT(bar_s_full0 + 8);
                             }
                             GNA_COMMIT(bar_kv_empty(slotK));
+                            // Q buffer free once the item's last QK^T completes
+                            if (C::EARLY_Q && j + 2 == nst) GNA_COMMIT(bar_qfree(b));
                         }
                     }
                     ++ni[0];
@@ -450,15 +457,18 @@ __global__ void __launch_bounds__(384, 1)
         int sph = 0;  // stages consumed (S barrier phase)
         int ni = 0;   // items processed by this WG (O barrier phase)
         int kq = 0;
+        int nuse = 0;  // O staging buffer uses (both WGs) before the current item
         for (long long t = first; t < n_range; t += step, ++kq) {
             long long bh, widx;
             decode_w(p.work_begin + t, bh, widx);
             const int4 item = __ldg(p.items + widx);
             const int b = kq % C::QBUF;
             const int sub = i == 0 ? item.y : item.z;
-            // no sub-tile B in this item: nothing to compute.  WG 0 releases the Q buffer for both
-            // (arrival count 2): an early arrival from here could complete the phase of an item
-            // WG 0 is still working on when two B-less items follow each other
+            const int ost_use = nuse + i;  // this WG's use index of the shared O staging buffer
+            nuse += item.z >= 0 ? 2 : 1;
+            // no sub-tile B in this item: nothing to compute.  Without EARLY_Q WG 0 releases the Q
+            // buffer for both (arrival count 2): an early arrival from here could complete the phase
+            // of an item WG 0 is still working on when two B-less items follow each other
             if (sub < 0) continue;
             const int4* info = p.item_info + 3 * widx;
             const int nkv = __ldg(info).w;
@@ -550,7 +560,14 @@ __global__ void __launch_bounds__(384, 1)
                 if (r == 0 && j == 0) GTI(t, i == 0 ? 2 : 8);
                 ptx::tc_fence_after();
                 float s[128];
-#if GNA_LD_BATCH
+                auto mask_cols = [&](int c0, int c1) {
+                    if (!warp_full) {
+                        // one select per element
+#pragma unroll
+                        for (int c = c0; c < c1; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
+                    }
+                };
+                float m_tile;
                 // all four 32-column loads in flight at once, one wait (the register fences pin
                 // every use of s after the wait)
 #pragma unroll
@@ -558,37 +575,40 @@ __global__ void __launch_bounds__(384, 1)
                 ptx::tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < 4; ++c) ptx::reg_fence32(&s[c * 32]);
-#else
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t rr[32];
-                    ptx::tmem_ld32(tS + c * 32, rr);
-                    ptx::tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(rr[e]);
-                }
-#endif
                 if (r == 0) GT(j, 4 * i + 1);
-                if (!warp_full) {
-                    // one select per element
+                mask_cols(0, 128);
+                {
+                    float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
 #pragma unroll
-                    for (int c = 0; c < 128; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
+                    for (int c = 4; c < 128; c += 8) {
+                        mx0 = ptx::max3(mx0, s[c], s[c + 1]);
+                        mx1 = ptx::max3(mx1, s[c + 2], s[c + 3]);
+                        mx2 = ptx::max3(mx2, s[c + 4], s[c + 5]);
+                        mx3 = ptx::max3(mx3, s[c + 6], s[c + 7]);
+                    }
+                    m_tile = ptx::max3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
                 }
                 constexpr int CH = 64 / GNA_PSPLIT;  // key pairs per P chunk
                 float la0 = 0.f, la1 = 0.f, lb0 = 0.f, lb1 = 0.f;
                 uint32_t pk[64];
-                auto do_pair = [&](int pi, float neg) {
-                    // x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU or, for 1 pair in GNA_POLY_EVERY, on
-                    // the FMA pipe (polynomial); row sum with FADD2; pack to bf16x2 / f16x2 (or E4M3, 4
-                    // keys per column)
-                    float x0, x1, y0, y1;
+                // 2^x of key pair pi: x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU or, for 1 pair in
+                // GNA_POLY_EVERY, on the FMA pipe (polynomial)
+                auto exp_pair = [&](int pi, float neg, float& y0, float& y1) {
+                    float x0, x1;
                     ptx::ffma2(x0, x1, s[2 * pi], s[2 * pi + 1], sl2, sl2, neg, neg);
+#ifdef GNA_POLY_MASK
+                    if ((GNA_POLY_MASK >> (pi & 7)) & 1) {  // pairs pi with bit (pi mod 8) set: polynomial
+#else
                     if (GNA_POLY_EVERY > 0 && (pi % (GNA_POLY_EVERY > 0 ? GNA_POLY_EVERY : 1)) == GNA_POLY_EVERY - 1) {
+#endif
                         ptx::ex2_poly2(y0, y1, x0, x1);
                     } else {
                         y0 = ptx::ex2(x0);
                         y1 = ptx::ex2(x1);
                     }
+                };
+                // row sum (FADD2) and pack of pair pi to bf16x2 / f16x2 (or E4M3, 4 keys per column)
+                auto fin_pair = [&](int pi, float y0, float y1) {
                     if (pi & 1) ptx::fadd2(lb0, lb1, lb0, lb1, y0, y1);
                     else ptx::fadd2(la0, la1, la0, la1, y0, y1);
                     if constexpr (F8) {
@@ -601,20 +621,9 @@ __global__ void __launch_bounds__(384, 1)
                         pk[pi] = ptx::pack_bf16x2(y0, y1);
                     }
                 };
-                auto tile_max = [&]() {
-                    float mx0 = s[0], mx1 = s[1], mx2 = s[2], mx3 = s[3];
-#pragma unroll
-                    for (int c = 4; c < 128; c += 8) {
-                        mx0 = ptx::max3(mx0, s[c], s[c + 1]);
-                        mx1 = ptx::max3(mx1, s[c + 2], s[c + 3]);
-                        mx2 = ptx::max3(mx2, s[c + 4], s[c + 5]);
-                        mx3 = ptx::max3(mx3, s[c + 6], s[c + 7]);
-                    }
-                    return ptx::max3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
-                };
                 // store the P columns of the chunk ending at pair pi (keys [2*(pi+1-CH), 2*(pi+1))) and,
-                // except for the last chunk, let the MMA start the PV on them right away
-                auto store_chunk = [&](int pi) {
+                // except for the last chunk, let the MMA start the PV on them
+                auto store_only = [&](int pi) {
                     const int c0 = pi + 1 - CH;
                     if constexpr (F8) {
                         if (CH == 64) ptx::tmem_st32(tS, *reinterpret_cast<const uint32_t(*)[32]>(&pk[0]));
@@ -625,13 +634,14 @@ __global__ void __launch_bounds__(384, 1)
                         ptx::tmem_st32(tS + c0, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0]));
                         ptx::tmem_st32(tS + c0 + 32, *reinterpret_cast<const uint32_t(*)[32]>(&pk[c0 + 32]));
                     }
-                    if (pi < 63) {
-                        ptx::tmem_wait_st();
-                        ptx::tc_fence_before();
-                        ptx::mbar_arrive(bar_pc0 + 8 * (3 * i + pi / CH));
-                    }
                 };
-                const float m_tile = tile_max();
+                auto release_chunk = [&](int chunk) {
+                    if (r == 0 && i == 0 && chunk == 0) GT(j, 14);
+                    ptx::tmem_wait_st();
+                    if (r == 0 && i == 0 && chunk == 0 && j > 0) GT(j, 15);
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(bar_pc0 + 8 * (3 * i + chunk));
+                };
                 const float m_new = fmaxf(m_used, m_tile);
                 if (r == 0) GT(j, 4 * i + 2);
                 // lazy max: O (and l) are rescaled only when some row's max grows by > 2^8
@@ -653,19 +663,27 @@ __global__ void __launch_bounds__(384, 1)
                     m_used = m_new;
                 }
                 const float neg = m_used == -INFINITY ? 0.f : -m_used;
+                // software-pipelined by GNA_EXP_LAG pairs: the sum / pack of pair pi - LAG issue after
+                // the exponentials of pair pi, so the MUFU latency is not exposed pair by pair
+                constexpr int LAG = GNA_EXP_LAG, LAGB = GNA_EXP_LAG + 1;
+                float yr[LAGB][2];
 #pragma unroll
-                for (int pi = 0; pi < CH; ++pi) do_pair(pi, neg);
-                store_chunk(CH - 1);
-#pragma unroll
-                for (int pi = CH; pi < 64; ++pi) {
-                    do_pair(pi, neg);
-                    if (pi % CH == CH - 1) store_chunk(pi);
+                for (int t = 0; t < 64 + LAG; ++t) {
+                    if (t < 64) exp_pair(t, neg, yr[t % LAGB][0], yr[t % LAGB][1]);
+                    const int pi = t - LAG;
+                    if (pi >= 0) {
+                        fin_pair(pi, yr[pi % LAGB][0], yr[pi % LAGB][1]);
+                        if (pi % CH == CH - 1) {
+                            store_only(pi);
+                            if (pi < 63) release_chunk(pi / CH);
+                        }
+                    }
                 }
-                l_run += (la0 + la1) + (lb0 + lb1);
                 ptx::tmem_wait_st();
                 if (r == 0) GT(j, 4 * i + 3);
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(bar_p);
+                l_run += (la0 + la1) + (lb0 + lb1);
             }
             if (r == 0 && i == 0) GTL(3);
             if (r == 0 && i == 0) GTI(t, 3);
@@ -735,7 +753,18 @@ __global__ void __launch_bounds__(384, 1)
                 // in the SW128 layout of a Q tile, then TMA-stored box by box (coalesced; the 5-D map
                 // clips rows past the grid edges).  E4M3: a Q tile is half a bf16 O tile, so O goes to
                 // a dedicated staging area.
-                const uint32_t sO = F8 ? sbase + C::OST_OFF + i * 2 * C::CHUNK_BYTES : sQ + (2 * b + i) * C::TILE_BYTES;
+                constexpr bool kShared = !F8 && C::EARLY_Q;
+                const uint32_t sO = F8       ? sbase + C::OST_OFF + i * 2 * C::CHUNK_BYTES
+                                    : kShared ? sbase + C::OST_OFF
+                                              : sQ + (2 * b + i) * C::TILE_BYTES;
+                if (kShared && ost_use >= 1) {
+                    // the previous user's TMA store has read the buffer.  A parity wait is exact here:
+                    // uses alternate A, B, A, ... (B possibly absent), so this WG's previous use was
+                    // use - 1 or use - 2, released before this thread got here (program order; the
+                    // WG's warps cannot drift by a whole item: every stage needs all 128 P arrivals),
+                    // hence the barrier is at phase use - 1 or use, never behind.
+                    ptx::mbar_wait(bar_ost, (ost_use - 1) & 1);
+                }
 #pragma unroll
                 for (int c = 0; c < DP / 32; ++c) {
                     const uint32_t rowb = sO + (c >> 1) * C::CHUNK_BYTES + r * 128;
@@ -767,12 +796,13 @@ __global__ void __launch_bounds__(384, 1)
                         }
                     }
                     ptx::bulk_commit();
-                    ptx::bulk_wait_read0();  // smem read by the TMA: the Q buffer may be refilled
-                    ptx::mbar_arrive_cnt(bar_qfree(b), item_e.z >= 0 ? 1u : 2u);
+                    ptx::bulk_wait_read0();  // smem read by the TMA: the staging buffer may be refilled
+                    if (!C::EARLY_Q) ptx::mbar_arrive_cnt(bar_qfree(b), item_e.z >= 0 ? 1u : 2u);
+                    else if (kShared) ptx::mbar_arrive(bar_ost);
                 }
                 if (F8) asm volatile("bar.sync %0, 128;" ::"r"(1 + i) : "memory");  // staging area reused next item
             } else {
-                if (r == 0) ptx::mbar_arrive_cnt(bar_qfree(b), item_e.z >= 0 ? 1u : 2u);
+                if (!C::EARLY_Q && r == 0) ptx::mbar_arrive_cnt(bar_qfree(b), item_e.z >= 0 ? 1u : 2u);
                 if (valid) {
 #pragma unroll
                     for (int c = 0; c < DP / 32; ++c) {

@@ -58,6 +58,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         if (n == (1ll << 25)) asm volatile("trap;");
     }
 }
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t) { mbar_wait(bar, parity); }
 #else
 #define GNA_PROG(slot, val) \
     do {                    \
@@ -77,6 +78,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(bar),
         "r"(parity)
         : "memory");
+}
+// Wait for a phase off the critical path (the producer warps): between polls the warp sleeps
+// `ns` nanoseconds instead of re-issuing try_wait, so it leaves the SMSP's issue slots to the
+// softmax warps that share it (a spinning producer took ~17% of its SMSP's issue slots, ncu).
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+    if (ns == 0) return mbar_wait(bar, parity);
+    for (;;) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+    }
 }
 #endif
 

@@ -14,6 +14,7 @@ cases = [
     ((64, 64), (32, 32), (16, 16), 1, 4, 128),
     ((12, 20, 18), (5, 8, 6), (2, 3, 6), 2, 2, 64),
 ]
+bad = 0
 for spatial, window, stride, B, H, D in cases:
     q, k, v = make_qkv(B, spatial, H, D, discriminating=True)
     t0 = time.time()
@@ -25,3 +26,5 @@ for spatial, window, stride, B, H, D in cases:
     e = np.abs(o - ro)
     print(spatial, window, stride, D, f"O max {np.nanmax(e):.3e} mean {np.nanmean(e):.3e} nan {np.isnan(o).sum()} "
           f"LSE max {np.nanmax(np.abs(l-rl)):.3e}  t={dt:.2f}s", flush=True)
+    bad += int(not (np.nanmax(e) <= 2e-2 and np.nanmax(np.abs(l - rl)) <= 1e-3 and not np.isnan(o).any()))
+sys.exit(1 if bad else 0)

@@ -6,7 +6,7 @@ import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2504_16922_b200 import build
 import paper_2504_16922_b200.gna as G
-G.LIB_PATH = build.build(trace=True)
+G.LIB_PATH = os.environ.get("TRACE_LIB") or build.build(trace=True)
 import numpy as np, torch
 import paper_2504_16922_b200 as gna
 from gna_inputs import WORKLOADS, make_qkv
@@ -61,6 +61,9 @@ for cta in range(2):
     s0 = s0[s0 > 0]
     if len(s0) > 8:
         d = np.diff(s0[4:])
+        med = lambda a, b: int(np.median((buf[cta, 4:len(s0), b] - buf[cta, 4:len(s0), a]).astype(np.int64)))
+        print("  chunk0: max->st issue", med(2, 14), "st wait", med(14, 15), "-> P0st", med(15, 3),
+              "; P0st->P0rdy", med(3, 9), "P0rdy->Knext", med(9, 11), "S1rdy-S0rdy", med(0, 4))
         print("  S0 period median", int(np.median(d)), "cycles;  softmax0 ld", int(np.median((buf[cta,4:len(s0),1]-buf[cta,4:len(s0),0]).astype(np.int64))),
               "max", int(np.median((buf[cta,4:len(s0),2]-buf[cta,4:len(s0),1]).astype(np.int64))),
               "exp+st", int(np.median((buf[cta,4:len(s0),3]-buf[cta,4:len(s0),2]).astype(np.int64))))
