@@ -381,7 +381,7 @@ std::shared_ptr<Plan> get_plan(const gna_args* a) {
 }
 
 // Host side of the work list: [items: n int4] then [info: 3 int4 per item] = {lo0, lo1, lo2, nkv},
-// {ext0, ext1, ext2, 0}, {class coords c0, c1, c2, 0}: the union KV box range of the item's
+// {ext0, ext1, ext2, dense}, {class coords c0, c1, c2, 0}: the union KV box range of the item's
 // sub-tiles, decoded once on the host so the kernel's prologue has no integer divisions before
 // its first TMA load.  Kept in pinned memory for the lifetime of the plan (async upload source).
 int plan_host_items(Plan& p) {
@@ -405,9 +405,24 @@ int plan_host_items(Plan& p) {
         }
         int cc[3];
         class_coords(p.g, it.x, cc);
+        // dense item: every box of the union range is full for every in-bounds query of
+        // each sub-tile, and the stages hold whole boxes only -- the softmax then skips the per-stage
+        // mask logic (perfectly block-sparse configs: every item)
+        const int nkv = (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]);
+        bool dense = nkv % (128 / p.g.box_vol) == 0;
+        for (int t = 0; t < (it.z >= 0 ? 2 : 1) && dense; ++t) {
+            int sc[3];
+            sub_coords(p.g, t == 0 ? it.y : it.z, sc);
+            for (int a = 0; a < 3 && dense; ++a) {
+                const int Lc = class_extent(p.g.ax[a], cc[a]);
+                const int ext = p.g.QB[a] * p.g.B[a];
+                for (int b = lo[a]; b < hi[a] && dense; ++b)
+                    dense = box_full(p.g.ax[a], Lc, sc[a] * ext, (sc[a] + 1) * ext, b, p.g.B[a]);
+            }
+        }
         h[i] = it;
-        h[n + 3 * i] = make_int4(lo[0], lo[1], lo[2], (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]));
-        h[n + 3 * i + 1] = make_int4(hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], 0);
+        h[n + 3 * i] = make_int4(lo[0], lo[1], lo[2], nkv);
+        h[n + 3 * i + 1] = make_int4(hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2], dense ? 1 : 0);
         h[n + 3 * i + 2] = make_int4(cc[0], cc[1], cc[2], 0);
     }
     p.host_items = h;

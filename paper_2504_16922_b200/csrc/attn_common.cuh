@@ -70,6 +70,15 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
                        // staged for its TMA store in a dedicated buffer), so the next item's Q loads
                        // while the current item's last stage and epilogue run
 #endif
+#ifndef GNA_B_DELAY
+#define GNA_B_DELAY 0  // sub-tile B's first QK^T of an item: 0 right after A's, 1 after A's first P chunk, 2 after A's P
+#endif
+#ifndef GNA_EXP_MUTEX
+#define GNA_EXP_MUTEX 0  // 1: the two softmax warpgroups run their exp loops in strict alternation
+#endif
+#ifndef GNA_DENSE_ITEMS
+#define GNA_DENSE_ITEMS 1  // 1: items whose every box is full skip the per-stage mask logic
+#endif
 #ifndef GNA_QWAIT_NS
 #define GNA_QWAIT_NS 256  // sleep between polls of the Q producer's "Q buffer free" wait
 #endif

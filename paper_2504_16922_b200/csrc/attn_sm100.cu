@@ -147,6 +147,8 @@ __global__ void __launch_bounds__(384, 1)
     // shared O staging buffer released by its TMA store (16-bit types, EARLY_Q): one phase per use,
     // uses in item order, sub-tile A before B
     const uint32_t bar_ost = bar0 + 32u + 16u * C::NS + 64u + 48u + 8u;
+    // GNA_EXP_MUTEX: exp-phase token, WG 0 may start (arrived by WG 1's 4 warps) / WG 1 may start
+    const uint32_t bar_tok0 = bar_ost + 8u, bar_tok1 = bar_ost + 16u;
 
     if (threadIdx.x == 0) {
         GT(0, 15);
@@ -174,6 +176,8 @@ __global__ void __launch_bounds__(384, 1)
         }
         for (int c = 0; c < 6; ++c) ptx::mbar_init(bar_pc0 + 8 * c, 128);
         ptx::mbar_init(bar_ost, 1);
+        ptx::mbar_init(bar_tok0, 4);
+        ptx::mbar_init(bar_tok1, 4);
         ptx::fence_mbar_init();
     }
     if (warp == 8) {
@@ -392,6 +396,11 @@ __global__ void __launch_bounds__(384, 1)
                     issue_qk(0, q16a, slotK * TILE16);
                     GNA_COMMIT(bar_s_full0);
                     if (hasB) {
+                        // GNA_B_DELAY: start sub-tile B's pipeline later (after A's first P chunk / full P
+                        // of stage 0) so the two softmax warpgroups' exp phases, which share the SMSPs'
+                        // MUFU units, overlap less (the steady-state A/B offset keeps the initial one)
+                        if (GNA_B_DELAY == 1 && GNA_PSPLIT > 1) ptx::mbar_wait(bar_pc0, pc[0] & 1);
+                        if (GNA_B_DELAY == 2) ptx::mbar_wait(bar_p_full0, pc[0] & 1);
                         issue_qk(1, q16b, slotK * TILE16);
                         GNA_COMMIT(bar_s_full0 + 8);
                     }
@@ -458,6 +467,7 @@ __global__ void __launch_bounds__(384, 1)
         int ni = 0;   // items processed by this WG (O barrier phase)
         int kq = 0;
         int nuse = 0;  // O staging buffer uses (both WGs) before the current item
+        int nturn = 0;  // exp phases this WG ran in two-sub-tile items (GNA_EXP_MUTEX token phases)
         for (long long t = first; t < n_range; t += step, ++kq) {
             long long bh, widx;
             decode_w(p.work_begin + t, bh, widx);
@@ -495,6 +505,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
 
+            const bool dense_item = GNA_DENSE_ITEMS && __ldg(info + 1).w != 0;
             float m_used = -INFINITY;
             float l_run = 0.f;
             BoxCursor cur;
@@ -509,7 +520,9 @@ __global__ void __launch_bounds__(384, 1)
                 // the 128 S registers; all ones when every row of the warp covers every key
                 bool warp_full;
                 uint32_t mw[4] = {~0u, ~0u, ~0u, ~0u};
-                if (j >= nst_gna) {
+                if (j < nst_gna && dense_item) {
+                    warp_full = true;  // every box of the item is full for every row: no mask logic
+                } else if (j >= nst_gna) {
                     // extra stages: dense, only the tail past n_extra is masked (uniform)
                     const int extra_left = p.n_extra - (j - nst_gna) * 128;
                     warp_full = extra_left >= 128;
@@ -663,6 +676,16 @@ __global__ void __launch_bounds__(384, 1)
                     m_used = m_new;
                 }
                 const float neg = m_used == -INFINITY ? 0.f : -m_used;
+                // GNA_EXP_MUTEX: the two warpgroups' exp loops (which share the SMSPs' MUFU units) run in
+                // strict alternation A(j), B(j), A(j+1), ... in items with both sub-tiles
+                const bool tok = GNA_EXP_MUTEX && item.z >= 0;
+                if (tok) {
+                    if (i == 0) {
+                        if (nturn > 0) ptx::mbar_wait(bar_tok0, (nturn - 1) & 1);
+                    } else {
+                        ptx::mbar_wait(bar_tok1, nturn & 1);
+                    }
+                }
                 // software-pipelined by GNA_EXP_LAG pairs: the sum / pack of pair pi - LAG issue after
                 // the exponentials of pair pi, so the MUFU latency is not exposed pair by pair
                 constexpr int LAG = GNA_EXP_LAG, LAGB = GNA_EXP_LAG + 1;
@@ -678,6 +701,11 @@ __global__ void __launch_bounds__(384, 1)
                             if (pi < 63) release_chunk(pi / CH);
                         }
                     }
+                }
+                if (tok) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(i == 0 ? bar_tok1 : bar_tok0);
+                    ++nturn;
                 }
                 ptx::tmem_wait_st();
                 if (r == 0) GT(j, 4 * i + 3);

@@ -1,0 +1,5 @@
+#!/bin/bash
+V=paper_2504_16922_b200/variants
+for v in mx mxm88; do GNA_LIB_PATH=$V/libgna_$v.so timeout 120 python scripts/dbg_small.py > /dev/null 2>&1 || { echo "SMOKE $v FAILED"; exit 1; }; done
+echo "== t_mx"; TRACE_LIB=$V/libgna_t_mx.so timeout 200 python scripts/trace_attn.py c4a_hunyuan_blocked 2>&1 | grep -A1 "chunk0" | head -2
+AB_REPS=2 timeout 1500 python scripts/ab.py run c4a_hunyuan_blocked,c2b_flux64_s16 base mx mxm88 mxl2 mxp16
