@@ -201,10 +201,9 @@ __global__ void __launch_bounds__(384, 1)
                 // NEXT-2): a 5-D box {64 cols, 1 head, B2, B1, B0 tokens} of the user's
                 // heads-last tensor with element strides = dilation, so the TMA gathers the
                 // class sub-grid itself and zero-fills past the tensor edges.
-                auto load_box = [&](const CUtensorMap* tm, uint32_t dst, uint32_t bar, long long bh, int cls,
-                                    const int* ccls, int k0, int k1, int k2) {
-                    const int b_idx = static_cast<int>(bh / g.heads);
-                    const int h_idx = static_cast<int>(bh - static_cast<long long>(b_idx) * g.heads);
+                // (b_idx, h_idx) = (bh / heads, bh % heads), decoded once per item by the caller
+                auto load_box = [&](const CUtensorMap* tm, uint32_t dst, uint32_t bar, long long bh, int b_idx,
+                                    int h_idx, int cls, const int* ccls, int k0, int k1, int k2) {
                     if (p.direct) {
                         const int c2 = ccls[2] + g.ax[2].d * k2 * g.B[2];
                         const int c3 = ccls[1] + g.ax[1].d * k1 * g.B[1];
@@ -241,6 +240,8 @@ __global__ void __launch_bounds__(384, 1)
                             if (t < GNA_TL_CTAS) g_gna_ti[t][7] = smid;
                         }
 #endif
+                        const int qb_idx = static_cast<int>(bh / g.heads);
+                        const int qh_idx = static_cast<int>(bh - static_cast<long long>(qb_idx) * g.heads);
                         for (int i = 0; i < (hasB ? 2 : 1); ++i) {
                             int sc[3];
                             sub_coords(g, i == 0 ? item.y : item.z, sc);
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(384, 1)
                                 // box u of the sub-tile, row-major over the sub-tile's QB box block
                                 const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
                                 load_box(&tmap_q, sQ + (2 * b + i) * C::TILE_BYTES + u * BV * 128, bar_q(b), bh,
-                                         item.x, ccl, sc[0] * g.QB[0] + u0, sc[1] * g.QB[1] + u1,
+                                         qb_idx, qh_idx, item.x, ccl, sc[0] * g.QB[0] + u0, sc[1] * g.QB[1] + u1,
                                          sc[2] * g.QB[2] + u2);
                             }
                         }
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(384, 1)
                                     const CUtensorMap* tm = kind == 0 ? &tmap_k : &tmap_v;
                                     for (int u = 0; u < KPB; ++u)
                                         load_box(tm, sKV + slot * C::TILE_BYTES + u * BV * 128, bar_kv_full(slot), bh,
-                                                 item.x, ccl, sb.k[u][0], sb.k[u][1], sb.k[u][2]);
+                                                 b_idx, h_idx, item.x, ccl, sb.k[u][0], sb.k[u][1], sb.k[u][2]);
                                 } else {
                                     // 128 extra tokens [b*T + e*128, +128) of head h; rows past T belong to the
                                     // next batch or are zero-filled, and are masked by the softmax
