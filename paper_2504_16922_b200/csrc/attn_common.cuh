@@ -79,6 +79,9 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
 #ifndef GNA_DENSE_ITEMS
 #define GNA_DENSE_ITEMS 1  // 1: items whose every box is full skip the per-stage mask logic
 #endif
+#ifndef GNA_MMA_BLOCK
+#define GNA_MMA_BLOCK 1  // 1: QK^T (8 MMAs) and PV halves (4 MMAs) issued from one asm block with one elect
+#endif
 #ifndef GNA_QWAIT_NS
 #define GNA_QWAIT_NS 256  // sleep between polls of the Q producer's "Q buffer free" wait
 #endif

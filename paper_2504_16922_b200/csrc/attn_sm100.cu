@@ -337,6 +337,10 @@ __global__ void __launch_bounds__(384, 1)
                 auto mk = [](uint32_t lo, uint32_t hi) { return (static_cast<uint64_t>(hi) << 32) | lo; };
                 constexpr uint32_t TILE16 = C::TILE_BYTES >> 4;
                 auto issue_qk = [&](int i, uint32_t q16, uint32_t k16) {
+                    if constexpr (GNA_MMA_BLOCK && !F8 && DP == 128) {
+                        ptx::mma_qk8_elect(i == 0 ? tS0 : tS1, loQ + q16, loK + k16, hiQK, IDESC_QK, 0u);
+                        return;
+                    }
                     // q16 / k16 laundered: the per-kk descriptors are formed here, not hoisted out of
                     // the stage loop into (spilled) registers
                     asm volatile("" : "+r"(q16), "+r"(k16));
@@ -352,6 +356,13 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 };
                 auto issue_pv = [&](int i, uint32_t v16, bool acc, int k0, int k1) {
+                    if constexpr (GNA_MMA_BLOCK && !F8) {
+                        if (k1 - k0 == 4) {
+                            ptx::mma_pv4_elect(i == 0 ? tO0 : tO1, (i == 0 ? tS0 : tS1) + k0 * 8,
+                                               loV + v16 + ((k0 * V_STEP) >> 4), hiV, IDESC_PV, acc ? 1u : 0u);
+                            return;
+                        }
+                    }
                     asm volatile("" : "+r"(v16));
                     const uint32_t vb = loV + v16;
 #pragma unroll

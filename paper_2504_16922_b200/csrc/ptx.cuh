@@ -273,6 +273,42 @@ __device__ __forceinline__ void mma_ss_elect(uint32_t d_tmem, uint64_t adesc, ui
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Block issue (kind::f16, one elect for the block): QK^T of one 128-row sub-tile over head_dim 128
+// = 8 SS MMAs, K step k at 16-byte offset OFF(k) = (k / 4) * 1024 + (k % 4) * 2 of both the A (Q) and
+// B (K) descriptors' start-address words a_lo / b_lo (shared high word hi); the first MMA accumulates
+// iff `acc`, the others always.  The descriptors are formed inside the block, so the issuing lane
+// needs one uniform base per operand instead of a register pair per MMA.
+#define GNA_QK8_STEP(OFF, P)                                                           \
+    "add.s32 la, %1, " #OFF ";\n\tadd.s32 lb, %2, " #OFF ";\n\t"                     \
+    "mov.b64 da, {la, %3};\n\tmov.b64 db, {lb, %3};\n\t"                              \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, " P ";\n\t"
+__device__ __forceinline__ void mma_qk8_elect(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
+                                              uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b32 la, lb;\n\t.reg .b64 da, db;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        GNA_QK8_STEP(0, "p") GNA_QK8_STEP(2, "t") GNA_QK8_STEP(4, "t") GNA_QK8_STEP(6, "t")
+        GNA_QK8_STEP(1024, "t") GNA_QK8_STEP(1026, "t") GNA_QK8_STEP(1028, "t") GNA_QK8_STEP(1030, "t")
+        "}" ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// PV of one sub-tile, 4 TS MMAs (K = 4 x 16 keys): A = P in TMEM at a_tmem + 8 k columns, B = V
+// with start-address word v_lo + 128 k (16 rows of 128 B per K step)
+#define GNA_PV4_STEP(K, P)                                                             \
+    "add.s32 lb, %2, " #K "*128;\n\tadd.s32 ta, %1, " #K "*8;\n\t"                     \
+    "mov.b64 db, {lb, %3};\n\t"                                                          \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], db, %4, " P ";\n\t"
+__device__ __forceinline__ void mma_pv4_elect(uint32_t d_tmem, uint32_t a_tmem, uint32_t v_lo, uint32_t hi,
+                                              uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p, t, e;\n\t.reg .b32 lb, ta;\n\t.reg .b64 db;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        GNA_PV4_STEP(0, "p") GNA_PV4_STEP(1, "t") GNA_PV4_STEP(2, "t") GNA_PV4_STEP(3, "t")
+        "}" ::"r"(d_tmem), "r"(a_tmem), "r"(v_lo), "r"(hi), "r"(idesc), "r"(acc)
+        : "memory");
+}
 // kind::f8f6f4 (E4M3 operands, fp32 accumulate; K = 32 per instruction), SURVEY NEXT-3
 __device__ __forceinline__ void mma_ss_f8_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                 uint32_t accumulate) {
