@@ -82,6 +82,15 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
 #ifndef GNA_MMA_BLOCK
 #define GNA_MMA_BLOCK 1  // 1: QK^T (8 MMAs) and PV halves (4 MMAs) issued from one asm block with one elect
 #endif
+#ifndef GNA_ODRAIN_BATCH
+#define GNA_ODRAIN_BATCH 1  // epilogue: the O columns loaded from TMEM with one wait
+#endif
+#ifndef GNA_SMEM_PAD
+#define GNA_SMEM_PAD 0  // extra (unused) dynamic smem bytes, for A/B of the L1 share
+#endif
+#ifndef GNA_PREFETCH_NEXT
+#define GNA_PREFETCH_NEXT 1  // the Q producer prefetches the next item's Q boxes into L2
+#endif
 #ifndef GNA_QWAIT_NS
 #define GNA_QWAIT_NS 256  // sleep between polls of the Q producer's "Q buffer free" wait
 #endif
@@ -122,7 +131,7 @@ struct Cfg {
     static constexpr int OST_OFF = KV_OFF + NS * TILE_BYTES;
     static constexpr int OST_BYTES = F8 ? 2 * 2 * CHUNK_BYTES : (EARLY_Q ? ONH * CHUNK_BYTES : 0);
     static constexpr int BAR_OFF = OST_OFF + OST_BYTES;
-    static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024;  // + barriers + alignment slack
+    static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024 + GNA_SMEM_PAD;  // + barriers + alignment slack
     static_assert(SMEM_BYTES <= 232448, "shared memory budget (227 KB per CTA)");
     static constexpr int THREADS = 384;
 };

@@ -219,6 +219,23 @@ __global__ void __launch_bounds__(384, 1)
                         for (int h = 0; h < C::NH; ++h) ptx::tma_load_2d(dst + h * C::CHUNK_BYTES, tm, bar, h * 64, row);
                     }
                 };
+                // L2 prefetch of one box (same coordinates as load_box, no smem, no completion)
+                auto prefetch_box = [&](const CUtensorMap* tm, long long bh, int b_idx, int h_idx, int cls,
+                                        const int* ccls, int k0, int k1, int k2) {
+                    if (p.direct) {
+                        const int c2 = ccls[2] + g.ax[2].d * k2 * g.B[2];
+                        const int c3 = ccls[1] + g.ax[1].d * k1 * g.B[1];
+                        const int c4 = b_idx * g.ax[0].L + ccls[0] + g.ax[0].d * k0 * g.B[0];
+#pragma unroll
+                        for (int h = 0; h < C::NH; ++h) ptx::tma_prefetch_5d(tm, h * 64, h_idx, c2, c3, c4);
+                    } else {
+                        const long long cls_row0 = ((bh * g.ncls + cls) * static_cast<long long>(g.nbox)) * BV;
+                        const int row =
+                            static_cast<int>(cls_row0 + static_cast<long long>((k0 * g.nb[1] + k1) * g.nb[2] + k2) * BV);
+#pragma unroll
+                        for (int h = 0; h < C::NH; ++h) ptx::tma_prefetch_2d(tm, h * 64, row);
+                    }
+                };
                 if (warp == 10) {
                     int kq = 0;
                     for (long long t = first; t < n_range; t += step, ++kq) {
@@ -251,6 +268,26 @@ __global__ void __launch_bounds__(384, 1)
                                 load_box(&tmap_q, sQ + (2 * b + i) * C::TILE_BYTES + u * BV * 128, bar_q(b), bh,
                                          qb_idx, qh_idx, item.x, ccl, sc[0] * g.QB[0] + u0, sc[1] * g.QB[1] + u1,
                                          sc[2] * g.QB[2] + u2);
+                            }
+                        }
+                        // GNA_PREFETCH_NEXT: the next item's Q boxes into L2 now, a whole item ahead of
+                        // their load (a cold 5-D Q gather of 128-byte rows took ~3 us on C2b)
+                        if (GNA_PREFETCH_NEXT && t + step < n_range) {
+                            long long nbh, nwidx;
+                            decode_w(p.work_begin + t + step, nbh, nwidx);
+                            const int4 nit = __ldg(p.items + nwidx);
+                            const int4 ncc4 = __ldg(p.item_info + 3 * nwidx + 2);
+                            const int nccl[3] = {ncc4.x, ncc4.y, ncc4.z};
+                            const int nb_idx = static_cast<int>(nbh / g.heads);
+                            const int nh_idx = static_cast<int>(nbh - static_cast<long long>(nb_idx) * g.heads);
+                            for (int i = 0; i < (nit.z >= 0 ? 2 : 1); ++i) {
+                                int sc[3];
+                                sub_coords(g, i == 0 ? nit.y : nit.z, sc);
+                                for (int u = 0; u < KPB; ++u) {
+                                    const int u2 = u % g.QB[2], u1 = (u / g.QB[2]) % g.QB[1], u0 = u / (g.QB[2] * g.QB[1]);
+                                    prefetch_box(&tmap_q, nbh, nb_idx, nh_idx, nit.x, nccl, sc[0] * g.QB[0] + u0,
+                                                 sc[1] * g.QB[1] + u1, sc[2] * g.QB[2] + u2);
+                                }
                             }
                         }
                     }
@@ -752,10 +789,24 @@ __global__ void __launch_bounds__(384, 1)
             const long long row_g =
                 cls_row0 + static_cast<long long>((bx[0] * g.nb[1] + bx[1]) * g.nb[2] + bx[2]) * BV + inner;
             ptx::mbar_wait(bar_o_full0 + 8 * i, ni & 1);
+            if (r == 0 && i == 0) GTI(t, 9);
             ptx::tc_fence_after();
             const float inv_l = (l_run > 0.f ? 1.0f / l_run : 0.f) * p.o_scale;
             // O/l packed to 16 bits in registers (4 x 16 words), then O_i is free for the next item
             uint32_t ov[DP / 2];
+#if GNA_ODRAIN_BATCH
+            {
+                // all DP/32 column loads in flight, one wait (reuses the S registers' budget)
+                float rr[DP];
+#pragma unroll
+                for (int c = 0; c < DP / 32; ++c) ptx::tmem_ld32f(tO + c * 32, &rr[c * 32]);
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < DP / 32; ++c) ptx::reg_fence32(&rr[c * 32]);
+#pragma unroll
+                for (int e = 0; e < DP / 2; ++e) ov[e] = pack_o<F16>(rr[2 * e] * inv_l, rr[2 * e + 1] * inv_l);
+            }
+#else
 #pragma unroll
             for (int c = 0; c < DP / 32; ++c) {
                 uint32_t rr[32];
@@ -765,8 +816,10 @@ __global__ void __launch_bounds__(384, 1)
                 for (int e = 0; e < 16; ++e)
                     ov[c * 16 + e] = pack_o<F16>(__uint_as_float(rr[2 * e]) * inv_l, __uint_as_float(rr[2 * e + 1]) * inv_l);
             }
+#endif
             ptx::tc_fence_before();
             ptx::mbar_arrive(bar_o_free0 + 8 * i);
+            if (r == 0 && i == 0) GTI(t, 10);
             // Output row: the permuted O row (stage API), or -- fused inverse permutation
             // -- the row of this token in the user's heads-last
             // layout [B][s0][s1][s2][H][D], so no separate unpermute pass is needed.
@@ -815,6 +868,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 ptx::fence_proxy_async_smem();
                 asm volatile("bar.sync %0, 128;" ::"r"(1 + i) : "memory");
+                if (r == 0 && i == 0) GTI(t, 11);
                 if (r == 0) {
 #pragma unroll
                     for (int u = 0; u < KPB; ++u) {
@@ -837,6 +891,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     ptx::bulk_commit();
                     ptx::bulk_wait_read0();  // smem read by the TMA: the staging buffer may be refilled
+                    if (i == 0) GTI(t, 12);
                     if (!C::EARLY_Q) ptx::mbar_arrive_cnt(bar_qfree(b), item_e.z >= 0 ? 1u : 2u);
                     else if (kShared) ptx::mbar_arrive(bar_ost);
                 }

@@ -45,6 +45,12 @@ q2s = (ev[:, 2] - ev[:, 0]) / 1000.0
 print(f"item Q issue -> S0 ready: mean {q2s.mean():.2f} us  max {q2s.max():.2f}")
 last_ep = (ev[:, 4] - ev[:, 3]) / 1000.0
 print(f"last P(A) -> epilogue A done: mean {last_ep.mean():.2f} us")
+has = ev[:, 12] > 0
+if has.any():
+    e = ev[has]
+    d = lambda a, b: ((e[:, b] - e[:, a]) / 1000.0).mean()
+    print(f"epilogue A phases (us): lastP->O full {d(3, 9):.2f}  O drain {d(9, 10):.2f}  staging+bar {d(10, 11):.2f}  "
+          f"TMA issue+read {d(11, 12):.2f}  ->done {d(12, 4):.2f}")
 gaps = []
 for s_, ns in per_sm.items():
     ns = sorted(ns, key=lambda n: ev[n, 2])
