@@ -97,8 +97,12 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
 #ifndef GNA_KVWAIT_NS
 #define GNA_KVWAIT_NS 64  // sleep between polls of the K/V producer's "ring slot free" wait
 #endif
+#ifndef GNA_EPI_OFFLOAD
+#define GNA_EPI_OFFLOAD 0  // 1: warp 11 issues the O TMA stores from per-sub-tile staging buffers, and the
+                           // Q buffer is released after the item's last QK^T (implies early Q release)
+#endif
 #ifndef GNA_NS128
-#define GNA_NS128 (GNA_QBUF == 2 ? 3 : 4)  // K/V ring slots of 32 KB at head_dim 128
+#define GNA_NS128 ((GNA_QBUF == 2 || GNA_EPI_OFFLOAD) ? 3 : 4)  // K/V ring slots of 32 KB at head_dim 128
 #endif
 #ifndef GNA_EXP_LAG
 #define GNA_EXP_LAG 0  // softmax exp loop software-pipelined by this many key pairs (0: sum/pack right behind)
@@ -124,12 +128,14 @@ struct Cfg {
     static constexpr int QBUF = GNA_QBUF;
     static constexpr int Q_OFF = 0;                  // QBUF buffers x 2 sub-tiles
     static constexpr int KV_OFF = 2 * QBUF * TILE_BYTES;
-    static constexpr bool EARLY_Q = GNA_EARLY_Q != 0;
+    static constexpr bool EPI_OFFLOAD = GNA_EPI_OFFLOAD != 0;
+    static constexpr bool EARLY_Q = GNA_EARLY_Q != 0 || EPI_OFFLOAD;
     static_assert(!EARLY_Q || QBUF == 1, "early Q release: one Q buffer (the O staging buffer takes the room)");
     // O staging for the TMA-store epilogue: E4M3 one bf16 O tile per sub-tile; 16-bit types with
     // EARLY_Q one O tile shared by the two sub-tiles (used in turn); otherwise O is staged in the Q buffer
     static constexpr int OST_OFF = KV_OFF + NS * TILE_BYTES;
-    static constexpr int OST_BYTES = F8 ? 2 * 2 * CHUNK_BYTES : (EARLY_Q ? ONH * CHUNK_BYTES : 0);
+    static constexpr int OST_TILE = F8 ? 2 * CHUNK_BYTES : ONH * CHUNK_BYTES;  // one bf16/fp16 O tile
+    static constexpr int OST_BYTES = (F8 || EPI_OFFLOAD) ? 2 * OST_TILE : (EARLY_Q ? ONH * CHUNK_BYTES : 0);
     static constexpr int BAR_OFF = OST_OFF + OST_BYTES;
     static constexpr int SMEM_BYTES = BAR_OFF + 512 + 1024 + GNA_SMEM_PAD;  // + barriers + alignment slack
     static_assert(SMEM_BYTES <= 232448, "shared memory budget (227 KB per CTA)");

@@ -130,6 +130,38 @@ __global__ void __launch_bounds__(384, 1)
         }
     };
 
+    // TMA stores of one staged O sub-tile (SW128 layout of a Q tile at smem address sO) of item
+    // (bh, class cls with coordinates cc, Q sub-tile sub): box by box, 2-D map over the permuted O
+    // rows (tma_store == 1) or the 5-D map over the user tensor (2)
+    auto store_o_tile = [&](uint32_t sO, long long bh, int cls, const int* cc, int sub) {
+        const Geometry& gg = p.g;
+        int sc[3];
+        sub_coords(gg, sub, sc);
+        const int b_idx = static_cast<int>(bh / gg.heads);
+        const int h_idx = static_cast<int>(bh - static_cast<long long>(b_idx) * gg.heads);
+        const long long cls_row0 = ((bh * gg.ncls + cls) * static_cast<long long>(gg.nbox)) * BV;
+#pragma unroll
+        for (int u = 0; u < C::KPB; ++u) {
+            const int v2 = u % gg.QB[2], v1 = (u / gg.QB[2]) % gg.QB[1], v0 = u / (gg.QB[2] * gg.QB[1]);
+            const int k0 = sc[0] * gg.QB[0] + v0, k1 = sc[1] * gg.QB[1] + v1, k2 = sc[2] * gg.QB[2] + v2;
+#pragma unroll
+            for (int h = 0; h < C::ONH; ++h) {
+                const uint32_t src = sO + u * BV * 128 + h * C::CHUNK_BYTES;
+                if (p.tma_store == 2) {
+                    const int c2 = cc[2] + gg.ax[2].d * k2 * gg.B[2];
+                    const int c3 = cc[1] + gg.ax[1].d * k1 * gg.B[1];
+                    const int c4 = b_idx * gg.ax[0].L + cc[0] + gg.ax[0].d * k0 * gg.B[0];
+                    ptx::tma_store_5d(&p.tmap_o, src, h * 64, h_idx, c2, c3, c4);
+                } else {
+                    const int row =
+                        static_cast<int>(cls_row0 + static_cast<long long>((k0 * gg.nb[1] + k1) * gg.nb[2] + k2) * BV);
+                    ptx::tma_store_2d(&p.tmap_o, src, h * 64, row);
+                }
+            }
+        }
+        ptx::bulk_commit();
+    };
+
     // ---------------------------------------------------------- smem carve
     const uint32_t sQ = sbase + C::Q_OFF;   // 2 buffers x (sub-tile A, sub-tile B)
     const uint32_t sKV = sbase + C::KV_OFF;
@@ -149,6 +181,9 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t bar_ost = bar0 + 32u + 16u * C::NS + 64u + 48u + 8u;
     // GNA_EXP_MUTEX: exp-phase token, WG 0 may start (arrived by WG 1's 4 warps) / WG 1 may start
     const uint32_t bar_tok0 = bar_ost + 8u, bar_tok1 = bar_ost + 16u;
+    // GNA_EPI_OFFLOAD: O tile i staged (128 softmax arrivals) / its staging buffer read by the TMA store
+    // (warp 11, 1 arrival)
+    const uint32_t bar_ostaged0 = bar_ost + 24u, bar_ofree0 = bar_ost + 40u;
 
     if (threadIdx.x == 0) {
         GT(0, 15);
@@ -178,6 +213,10 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mbar_init(bar_ost, 1);
         ptx::mbar_init(bar_tok0, 4);
         ptx::mbar_init(bar_tok1, 4);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(bar_ostaged0 + 8 * i, 128);
+            ptx::mbar_init(bar_ofree0 + 8 * i, 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 8) {
@@ -344,6 +383,31 @@ __global__ void __launch_bounds__(384, 1)
                         }
                     }
                 }
+            }
+        } else if (C::EPI_OFFLOAD && warp == 11) {
+            // ===================================================== O store issuer (GNA_EPI_OFFLOAD)
+            // the softmax warpgroups stage O and move on; this warp issues the TMA stores, waits for
+            // the staging buffer to be read and hands it back
+            if (p.tma_store) {
+                int nu[2] = {0, 0};
+                for (long long t = first; t < n_range; t += step) {
+                    long long bh, widx;
+                    decode_w(p.work_begin + t, bh, widx);
+                    const int4 item = __ldg(p.items + widx);
+                    const int4 cc4 = __ldg(p.item_info + 3 * widx + 2);
+                    const int cc[3] = {cc4.x, cc4.y, cc4.z};
+                    for (int i = 0; i < (item.z >= 0 ? 2 : 1); ++i) {
+                        ptx::mbar_wait_sleep(bar_ostaged0 + 8 * i, nu[i] & 1, 32);
+                        if (lane == 0) {
+                            store_o_tile(sbase + C::OST_OFF + i * C::OST_TILE, bh, item.x, cc, i == 0 ? item.y : item.z);
+                            ptx::bulk_wait_read0();
+                            ptx::mbar_arrive(bar_ofree0 + 8 * i);
+                        }
+                        __syncwarp();
+                        ++nu[i];
+                    }
+                }
+                if (lane == 0) ptx::bulk_wait_all0();  // global writes complete before the CTA exits
             }
         } else if (warp == 9) {
             // ======================================================= MMA issuer
@@ -841,7 +905,23 @@ __global__ void __launch_bounds__(384, 1)
                 lrow = p.lse_perm + row_g;
                 ncols = DP;
             }
-            if (p.tma_store) {
+            if (C::EPI_OFFLOAD && p.tma_store) {
+                // O staged in this sub-tile's own staging buffer (its previous use read by the TMA
+                // store of warp 11); the stores themselves are issued by warp 11
+                const uint32_t sO = sbase + C::OST_OFF + i * C::OST_TILE;
+                if (ni > 0) ptx::mbar_wait(bar_ofree0 + 8 * i, (ni - 1) & 1);
+#pragma unroll
+                for (int c = 0; c < DP / 32; ++c) {
+                    const uint32_t rowb = sO + (c >> 1) * C::CHUNK_BYTES + r * 128;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        ptx::sts128(rowb + ((((c & 1) * 4 + q) ^ (r & 7)) << 4), ov[c * 16 + 4 * q],
+                                    ov[c * 16 + 4 * q + 1], ov[c * 16 + 4 * q + 2], ov[c * 16 + 4 * q + 3]);
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::mbar_arrive(bar_ostaged0 + 8 * i);
+                if (r == 0 && i == 0) GTI(t, 11);
+            } else if (p.tma_store) {
                 // O staged in this sub-tile's Q buffer (free: every QK^T of the item has completed)
                 // in the SW128 layout of a Q tile, then TMA-stored box by box (coalesced; the 5-D map
                 // clips rows past the grid edges).  E4M3: a Q tile is half a bf16 O tile, so O goes to
