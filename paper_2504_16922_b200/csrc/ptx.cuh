@@ -31,6 +31,9 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+#ifndef GNA_WAIT_SUSPEND
+#define GNA_WAIT_SUSPEND 1000000  // producer waits: try_wait suspend-time hint in ns (0: poll + __nanosleep)
+#endif
 #ifdef GNA_HANG_DEBUG
 // debug build: per-CTA progress words written by the kernels (GNA_PROG), printed on a hang
 __device__ int g_prog[2048][8];
@@ -84,6 +87,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // softmax warps that share it (a spinning producer took ~17% of its SMSP's issue slots, ncu).
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
     if (ns == 0) return mbar_wait(bar, parity);
+#if GNA_WAIT_SUSPEND
+    // try_wait with a suspend-time hint: the warp is suspended until the phase completes (or the
+    // hint expires) instead of re-polling (__nanosleep may return at once: ncu counted ~200 polls
+    // per stage with 256 ns sleeps)
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAITS_%=;\n}" ::"r"(bar),
+        "r"(parity), "r"(GNA_WAIT_SUSPEND)
+        : "memory");
+    return;
+#endif
     for (;;) {
         uint32_t ok;
         asm volatile(

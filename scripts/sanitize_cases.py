@@ -25,6 +25,8 @@ CASES = [
     ("2d_permuted_unfused", dict(spatial=(40, 36), window=(9, 12), stride=(3, 4)), 128, GNA_FLAG_UNFUSED_EPILOGUE),
     ("3d_permuted_fused", dict(spatial=(12, 20, 18), window=(5, 8, 6), stride=(2, 3, 6), dilation=(1, 2, 1),
                                causal=(True, False, False)), 128, GNA_FLAG_PERMUTED),
+    # blocked (every item dense) with more work items (256) than SMs: the persistent multi-item path
+    ("3d_blocked_dense_persistent", dict(spatial=(16, 32, 32), window=(8, 16, 16), stride=(8, 16, 16)), 128, 0),
 ]
 
 
