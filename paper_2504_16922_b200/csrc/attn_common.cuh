@@ -89,7 +89,8 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
 #define GNA_SMEM_PAD 0  // extra (unused) dynamic smem bytes, for A/B of the L1 share
 #endif
 #ifndef GNA_PREFETCH_NEXT
-#define GNA_PREFETCH_NEXT 1  // the Q producer prefetches the next item's Q boxes into L2
+#define GNA_PREFETCH_NEXT 24  // the Q producer prefetches the next item's Q boxes into L2 when the current
+                              // item has at most this many 128-key stages (0: never)
 #endif
 #ifndef GNA_QWAIT_NS
 #define GNA_QWAIT_NS 256  // sleep between polls of the Q producer's "Q buffer free" wait

@@ -311,7 +311,10 @@ __global__ void __launch_bounds__(384, 1)
                         }
                         // GNA_PREFETCH_NEXT: the next item's Q boxes into L2 now, a whole item ahead of
                         // their load (a cold 5-D Q gather of 128-byte rows took ~3 us on C2b)
-                        if (GNA_PREFETCH_NEXT && t + step < n_range) {
+                        // (short items only: a long item would leave the prefetched lines in L2 long enough
+                        // to be evicted by its K/V stream -- +0.26 GB DRAM reads on C4a)
+                        if (GNA_PREFETCH_NEXT && t + step < n_range &&
+                            __ldg(p.item_info + 3 * widx).w <= GNA_PREFETCH_NEXT * KPB) {
                             long long nbh, nwidx;
                             decode_w(p.work_begin + t + step, nbh, nwidx);
                             const int4 nit = __ldg(p.items + nwidx);
