@@ -733,6 +733,7 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
         if (a->work_end > 0) we = a->work_end;
         if (wb < 0 || we > total || wb > we) return fail(GNA_EINVAL, "work range outside [0, n_work] or begin > end");
     }
+    if (we - wb >= (1LL << 31) - (1LL << 20)) return fail(GNA_EINVAL, "work range longer than 2^31 - 2^20 items: split the launch");
     p.work_begin = wb;
     p.work_end = we;
     p.o_perm = c.ws ? c.ws + c.L.o : nullptr;
@@ -743,6 +744,9 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
     p.fp16 = a->dtype == GNA_DTYPE_FP16 ? 1 : 0;
     p.num_sms = device_sms();
     p.o_scale = 1.0f;
+    for (int w = 0; w < 4; ++w) p.comb1[w] = p.comb0[w] = 0u;
+    for (int i = 0; i < c.g.B[1]; ++i) p.comb1[(i * c.g.B[2]) >> 5] |= 1u << ((i * c.g.B[2]) & 31);
+    for (int i = 0; i < c.g.B[0]; ++i) p.comb0[(i * c.g.B[1] * c.g.B[2]) >> 5] |= 1u << ((i * c.g.B[1] * c.g.B[2]) & 31);
     if (fp8) {  // per-tensor dequantisation: S scales by q_scale*k_scale, O by v_scale
         p.scale_log2 *= (a->q_scale > 0.f ? a->q_scale : 1.f) * (a->k_scale > 0.f ? a->k_scale : 1.f);
         p.o_scale = a->v_scale > 0.f ? a->v_scale : 1.f;

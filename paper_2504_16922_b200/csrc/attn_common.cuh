@@ -249,5 +249,25 @@ __device__ __forceinline__ u128 box_row_mask(const Geometry& g, const BoxMaskCon
     return (m12 * mc.comb0) & bit_range(a[0] * s01, b[0] * s01);
 }
 
+// The same row mask for a 64-token box in 64-bit arithmetic (half the instructions of the 128-bit
+// form: one-word shifts and multiplies).  comb1 / comb0 are the low words of the 128-bit constants.
+__device__ __forceinline__ uint64_t bits_below64(int n) {  // n in [0, 64]
+    return n >= 64 ? ~0ull : ((1ull << n) - 1);
+}
+__device__ __forceinline__ uint64_t box_row_mask64(const Geometry& g, uint64_t comb1, uint64_t comb0, const int lo[3],
+                                                   const int hi[3]) {
+    int a[3], b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a[k] = max(lo[k], 0);
+        b[k] = min(hi[k], g.B[k]);
+        if (a[k] >= b[k]) return 0;
+    }
+    const uint64_t m2 = bits_below64(b[2]) & ~bits_below64(a[2]);
+    const uint64_t m12 = (m2 * comb1) & bits_below64(b[1] * g.B[2]) & ~bits_below64(a[1] * g.B[2]);
+    const int s01 = g.B[1] * g.B[2];
+    return (m12 * comb0) & bits_below64(b[0] * s01) & ~bits_below64(a[0] * s01);
+}
+
 }  // namespace attn
 }  // namespace gna

@@ -115,8 +115,10 @@ __global__ void __launch_bounds__(384, 1)
     }
 
     // ---------------------------------------------------------- this CTA's items
-    const long long n_range = p.work_end - p.work_begin;
-    const long long first = blockIdx.x, step = gridDim.x;
+    // 32-bit item counters (the host limits a launch's range to < 2^31 - 2^20 items): fewer live
+    // registers in the 64-register control warps and across the softmax stage loop
+    const int n_range = static_cast<int>(p.work_end - p.work_begin);
+    const int first = blockIdx.x, step = gridDim.x;
     // global work index w -> (unit bh, item index widx)
     auto decode_w = [&](long long w, long long& bh, long long& widx) {
         if ((w | p.n_items) < (1LL << 31)) {
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(384, 1)
                 };
                 if (warp == 10) {
                     int kq = 0;
-                    for (long long t = first; t < n_range; t += step, ++kq) {
+                    for (int t = first; t < n_range; t += step, ++kq) {
                         long long bh, widx;
                         decode_w(p.work_begin + t, bh, widx);
                         const int4 item = __ldg(p.items + widx);
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(384, 1)
                     uint32_t ph = 0;
                     bool first_load = true;
                     StageBoxes sb;
-                    for (long long t = first; t < n_range; t += step) {
+                    for (int t = first; t < n_range; t += step) {
                         long long bh, widx;
                         decode_w(p.work_begin + t, bh, widx);
                         const int4 item = __ldg(p.items + widx);
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(384, 1)
             // the staging buffer to be read and hands it back
             if (p.tma_store) {
                 int nu[2] = {0, 0};
-                for (long long t = first; t < n_range; t += step) {
+                for (int t = first; t < n_range; t += step) {
                     long long bh, widx;
                     decode_w(p.work_begin + t, bh, widx);
                     const int4 item = __ldg(p.items + widx);
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(384, 1)
                 int pc[2] = {0, 0};   // stages consumed per sub-tile (P barrier phases)
                 int ni[2] = {0, 0};   // items seen per sub-tile (O barrier phases)
                 int kq = 0;
-                for (long long t = first; t < n_range; t += step, ++kq) {
+                for (int t = first; t < n_range; t += step, ++kq) {
                     long long bh, widx;
                     decode_w(p.work_begin + t, bh, widx);
                     const int4 item = __ldg(p.items + widx);
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(384, 1)
         int kq = 0;
         int nuse = 0;  // O staging buffer uses (both WGs) before the current item
         int nturn = 0;  // exp phases this WG ran in two-sub-tile items (GNA_EXP_MUTEX token phases)
-        for (long long t = first; t < n_range; t += step, ++kq) {
+        for (int t = first; t < n_range; t += step, ++kq) {
             long long bh, widx;
             decode_w(p.work_begin + t, bh, widx);
             const int4 item = __ldg(p.items + widx);
@@ -634,15 +636,18 @@ __global__ void __launch_bounds__(384, 1)
                 // 128-bit row mask of the stage (1 or 2 boxes, or the extra tokens), built from the
                 // row's coordinates BEFORE S is loaded, so the mask arithmetic is not live next to
                 // the 128 S registers; all ones when every row of the warp covers every key
-                bool warp_full;
+                // mfull[h]: every row of the warp covers every key of stage half h (keys [64h, 64h+64),
+                // one box when the box holds 64 tokens): that half needs no per-element select
+                bool mfull[2] = {true, true};
                 uint32_t mw[4] = {~0u, ~0u, ~0u, ~0u};
                 if (j < nst_gna && dense_item) {
-                    warp_full = true;  // every box of the item is full for every row: no mask logic
+                    // every box of the item is full for every row: no mask logic
                 } else if (j >= nst_gna) {
                     // extra stages: dense, only the tail past n_extra is masked (uniform)
                     const int extra_left = p.n_extra - (j - nst_gna) * 128;
-                    warp_full = extra_left >= 128;
-                    if (!warp_full) {
+                    mfull[0] = extra_left >= 64;
+                    mfull[1] = extra_left >= 128;
+                    if (!mfull[1]) {
                         const u128 m = bits_below(extra_left);  // keys [0, n_extra - e*128)
                         mw[0] = static_cast<uint32_t>(m);
                         mw[1] = static_cast<uint32_t>(m >> 32);
@@ -658,11 +663,11 @@ __global__ void __launch_bounds__(384, 1)
                         const int ext[3] = {inf_ext.x, inf_ext.y, inf_ext.z};
                         cur.stage(lo, ext, nkv, KPB, sb);
                     }
-                    // per-row coverage of every key of the stage; padded rows never mask
-                    bool row_full = true;
+                    // per-row coverage of every key of each box; padded rows never mask
                     int rlo[KPB][3], rhi[KPB][3];
 #pragma unroll
                     for (int u = 0; u < KPB; ++u) {
+                        bool row_full = true;
 #pragma unroll
                         for (int a = 0; a < 3; ++a) {
                             const int base = sb.k[u][a] * g.B[a];
@@ -670,16 +675,33 @@ __global__ void __launch_bounds__(384, 1)
                             rhi[u][a] = sb.dead[u] ? -1 : wen[a] - base;
                             row_full = row_full && rlo[u][a] <= 0 && rhi[u][a] >= g.B[a];
                         }
+                        mfull[u] = __all_sync(0xffffffffu, row_full || !valid);
                     }
-                    warp_full = __all_sync(0xffffffffu, row_full || !valid);
-                    if (!warp_full) {
-                        const BoxMaskConsts mconst = box_mask_consts(g);  // recomputed: not kept live
-                        u128 m = box_row_mask(g, mconst, rlo[0], rhi[0]);
-                        if (KPB == 2) m |= box_row_mask(g, mconst, rlo[KPB - 1], rhi[KPB - 1]) << 64;
-                        mw[0] = static_cast<uint32_t>(m);
-                        mw[1] = static_cast<uint32_t>(m >> 32);
-                        mw[2] = static_cast<uint32_t>(m >> 64);
-                        mw[3] = static_cast<uint32_t>(m >> 96);
+                    if (KPB == 1) mfull[1] = mfull[0];
+                    // the comb constants come precomputed with the launch parameters (uniform)
+                    const BoxMaskConsts mconst = {
+                        static_cast<u128>(p.comb1[0]) | (static_cast<u128>(p.comb1[1]) << 32) |
+                            (static_cast<u128>(p.comb1[2]) << 64) | (static_cast<u128>(p.comb1[3]) << 96),
+                        static_cast<u128>(p.comb0[0]) | (static_cast<u128>(p.comb0[1]) << 32) |
+                            (static_cast<u128>(p.comb0[2]) << 64) | (static_cast<u128>(p.comb0[3]) << 96)};
+#pragma unroll
+                    for (int u = 0; u < KPB; ++u) {
+                        if (!mfull[u]) {
+                            if constexpr (BV == 64) {
+                                const uint64_t m = box_row_mask64(
+                                    g, static_cast<uint64_t>(p.comb1[0]) | (static_cast<uint64_t>(p.comb1[1]) << 32),
+                                    static_cast<uint64_t>(p.comb0[0]) | (static_cast<uint64_t>(p.comb0[1]) << 32), rlo[u],
+                                    rhi[u]);
+                                mw[2 * u] = static_cast<uint32_t>(m);
+                                mw[2 * u + 1] = static_cast<uint32_t>(m >> 32);
+                            } else {
+                                const u128 m = box_row_mask(g, mconst, rlo[u], rhi[u]);
+                                mw[0] = static_cast<uint32_t>(m);
+                                mw[1] = static_cast<uint32_t>(m >> 32);
+                                mw[2] = static_cast<uint32_t>(m >> 64);
+                                mw[3] = static_cast<uint32_t>(m >> 96);
+                            }
+                        }
                     }
                 }
 
@@ -690,10 +712,14 @@ __global__ void __launch_bounds__(384, 1)
                 ptx::tc_fence_after();
                 float s[128];
                 auto mask_cols = [&](int c0, int c1) {
-                    if (!warp_full) {
-                        // one select per element
+                    // one select per element, only in the stage halves some row of the warp does not cover
 #pragma unroll
-                        for (int c = c0; c < c1; ++c) s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
+                    for (int h = 0; h < 2; ++h) {
+                        if (!mfull[h] && c0 < 64 * h + 64 && c1 > 64 * h) {
+#pragma unroll
+                            for (int c = (c0 > 64 * h ? c0 : 64 * h); c < (c1 < 64 * h + 64 ? c1 : 64 * h + 64); ++c)
+                                s[c] = ((mw[c >> 5] >> (c & 31)) & 1u) ? s[c] : -INFINITY;
+                        }
                     }
                 };
                 float m_tile;
@@ -834,8 +860,8 @@ __global__ void __launch_bounds__(384, 1)
 
             // ---------------------------------------------------------- epilogue
             // the row's position, recomputed from the (laundered) work index
-            long long t_e = t;
-            asm volatile("" : "+l"(t_e));
+            int t_e = t;
+            asm volatile("" : "+r"(t_e));
             decode_w(p.work_begin + t_e, bh, widx);
             const int4 item_e = __ldg(p.items + widx);
             const int4 cc4 = __ldg(p.item_info + 3 * widx + 2);

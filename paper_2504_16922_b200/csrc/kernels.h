@@ -31,6 +31,9 @@ struct AttnParams {
     int fp8;                // 1: Q/K/V are E4M3, per-tensor scales folded in below
     int fp16;               // 1: Q/K/V and O are fp16 (kind::f16 with F16 operands, P packed f16x2)
     float o_scale;          // O multiplier (v_scale for FP8, 1 for bf16)
+    // comb constants of the separable box row mask (attn_common.cuh box_row_mask), 128-bit, low word
+    // first: comb1 = bits i1*B2 (i1 < B1), comb0 = bits i0*B1*B2 (i0 < B0)
+    uint32_t comb1[4], comb0[4];
     CUtensorMap tmap_o;
 };
 
