@@ -62,6 +62,9 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
 #ifndef GNA_POLY_EVERY
 #define GNA_POLY_EVERY 8  // 1 exp pair in GNA_POLY_EVERY on the FMA pipe (0 = all MUFU)
 #endif
+#ifndef GNA_POLY_EVERY_F8
+#define GNA_POLY_EVERY_F8 GNA_POLY_EVERY  // the same for the E4M3 kernel (half the tensor time per exp)
+#endif
 #ifndef GNA_QBUF
 #define GNA_QBUF 1  // Q buffers (2: the next item's Q loads while the current item runs)
 #endif

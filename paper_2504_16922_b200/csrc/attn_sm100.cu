@@ -754,7 +754,8 @@ __global__ void __launch_bounds__(384, 1)
 #ifdef GNA_POLY_MASK
                     if ((GNA_POLY_MASK >> (pi & 7)) & 1) {  // pairs pi with bit (pi mod 8) set: polynomial
 #else
-                    if (GNA_POLY_EVERY > 0 && (pi % (GNA_POLY_EVERY > 0 ? GNA_POLY_EVERY : 1)) == GNA_POLY_EVERY - 1) {
+                    constexpr int POLY = F8 ? GNA_POLY_EVERY_F8 : GNA_POLY_EVERY;
+                    if (POLY > 0 && (pi % (POLY > 0 ? POLY : 1)) == POLY - 1) {
 #endif
                         ptx::ex2_poly2(y0, y1, x0, x1);
                     } else {
