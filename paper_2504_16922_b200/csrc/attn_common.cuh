@@ -63,7 +63,11 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
 #define GNA_POLY_EVERY 8  // 1 exp pair in GNA_POLY_EVERY on the FMA pipe (0 = all MUFU)
 #endif
 #ifndef GNA_POLY_EVERY_F8
-#define GNA_POLY_EVERY_F8 GNA_POLY_EVERY  // the same for the E4M3 kernel (half the tensor time per exp)
+#define GNA_POLY_EVERY_F8 16  // the E4M3 kernel: 1 pair in 16 (A/B ab16-ab17: fewer polynomial exps pay there)
+#endif
+#ifndef GNA_POLY_SCALE
+#define GNA_POLY_SCALE 1  // 1: polynomial exps apply 2^n by a multiplication that is exactly 0 at n = -127 (no select;
+                          // A/B ab19: C4a / X1 +1-2% TF/s, +3% per GHz; 0: compare-and-select form)
 #endif
 #ifndef GNA_QBUF
 #define GNA_QBUF 1  // Q buffers (2: the next item's Q loads while the current item runs)
@@ -81,6 +85,10 @@ static __device__ unsigned long long g_gna_ti[GNA_TL_CTAS][16];
 #endif
 #ifndef GNA_DENSE_ITEMS
 #define GNA_DENSE_ITEMS 1  // 1: items whose every box is full skip the per-stage mask logic
+#endif
+#ifndef GNA_DENSE_FOLD
+#define GNA_DENSE_FOLD 1  // 1: the dense-item flag folded into a stage count (one live value fewer in the stage
+                          // loop: the per-stage reload of the spilled flag goes away; A/B ab18 neutral)
 #endif
 #ifndef GNA_MMA_BLOCK
 #define GNA_MMA_BLOCK 1  // 1: QK^T (8 MMAs) and PV halves (4 MMAs) issued from one asm block with one elect

@@ -623,7 +623,13 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
 
+#if GNA_DENSE_FOLD
+            // stages [0, nst_dense) need no mask logic (all of the item's GNA stages when it is dense, else
+            // none); one int instead of a flag next to nst_gna, and nst_gna re-derived from nst
+            const int nst_dense = (GNA_DENSE_ITEMS && __ldg(info + 1).w != 0) ? nst_gna : 0;
+#else
             const bool dense_item = GNA_DENSE_ITEMS && __ldg(info + 1).w != 0;
+#endif
             float m_used = -INFINITY;
             float l_run = 0.f;
             BoxCursor cur;
@@ -640,7 +646,11 @@ __global__ void __launch_bounds__(384, 1)
                 // one box when the box holds 64 tokens): that half needs no per-element select
                 bool mfull[2] = {true, true};
                 uint32_t mw[4] = {~0u, ~0u, ~0u, ~0u};
+#if GNA_DENSE_FOLD
+                if (j < nst_dense) {
+#else
                 if (j < nst_gna && dense_item) {
+#endif
                     // every box of the item is full for every row: no mask logic
                 } else if (j >= nst_gna) {
                     // extra stages: dense, only the tail past n_extra is masked (uniform)
@@ -757,7 +767,8 @@ __global__ void __launch_bounds__(384, 1)
                     constexpr int POLY = F8 ? GNA_POLY_EVERY_F8 : GNA_POLY_EVERY;
                     if (POLY > 0 && (pi % (POLY > 0 ? POLY : 1)) == POLY - 1) {
 #endif
-                        ptx::ex2_poly2(y0, y1, x0, x1);
+                        if constexpr (GNA_POLY_SCALE) ptx::ex2_poly2s(y0, y1, x0, x1);
+                        else ptx::ex2_poly2(y0, y1, x0, x1);
                     } else {
                         y0 = ptx::ex2(x0);
                         y1 = ptx::ex2(x1);

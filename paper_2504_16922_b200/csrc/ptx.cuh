@@ -482,6 +482,34 @@ __device__ __forceinline__ void fadd2(float& d0, float& d1, float a0, float a1, 
         : "=f"(d0), "=f"(d1)
         : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
+__device__ __forceinline__ void fmul2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+// 2^x for a pair, as ex2_poly2 below but with the exponent applied as a multiplication by
+// 2^n built from n's bits: x is clamped to >= -127, and for n = -127 the 2^n bit pattern
+// ((n mod 512) << 23) + (127 << 23) wraps to exactly +0, so masked logits (x = -inf) give
+// exactly 0 without a compare and select (3 instructions fewer per pair).  Results agree
+// with ex2_poly2 bit for bit for x >= -126; below that both are < 2^-126.
+__device__ __forceinline__ void ex2_poly2s(float& y0, float& y1, float x0_in, float x1_in) {
+    const float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic holds round(x) in the low bits
+    const float x0 = fmaxf(x0_in, -127.0f);
+    const float x1 = fmaxf(x1_in, -127.0f);
+    float t0, t1, r0, r1, f0, f1, q0, q1;
+    fadd2(t0, t1, x0, x1, kMagic, kMagic);
+    fadd2(r0, r1, t0, t1, -kMagic, -kMagic);
+    fadd2(f0, f1, x0, x1, -r0, -r1);
+    ffma2(q0, q1, f0, f1, 0.055170836f, 0.055170836f, 0.24260935f, 0.24260935f);
+    ffma2(q0, q1, q0, q1, f0, f1, 0.69326096f, 0.69326096f);
+    ffma2(q0, q1, q0, q1, f0, f1, 0.99992818f, 0.99992818f);
+    const float s0 = __uint_as_float((__float_as_uint(t0) << 23) + 0x3F800000u);
+    const float s1 = __uint_as_float((__float_as_uint(t1) << 23) + 0x3F800000u);
+    fmul2(y0, y1, q0, q1, s0, s1);
+}
+
 // 2^x for a pair on the FMA/ALU pipes (offloads the MUFU unit): round-to-nearest
 // split x = n + f, f in [-0.5, 0.5], degree-3 minimax polynomial for 2^f (max rel.
 // error 7.5e-5, far below bf16's 2^-9), exponent added as n << 23.  The polynomial
