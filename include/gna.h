@@ -131,9 +131,7 @@ typedef struct gna_args {
     long long work_end;     /* the n_work = batch*heads*n_items items, unit-major (item w of
                                the launch = unit w / n_items, u = b*heads + h).  Without
                                GNA_FLAG_WORK_RANGE, end <= 0 -> to the end.  Outside
-                               [0, n_work] or begin > end: GNA_EINVAL.  A launch's range
-                               must hold fewer than 2^31 - 2^20 items (32-bit counters in the
-                               kernel), else GNA_EINVAL: split it into several launches. */
+                               [0, n_work] or begin > end: GNA_EINVAL. */
     int flags;
     /* Extra (text) KV tokens fused into the same kernel:
      * n_extra keys/values per (batch, head), layout [B][n_extra][H][D] in q's

@@ -733,7 +733,6 @@ int do_attention(const gna_args* a, Ctx& c, bool fused_out = false, bool direct 
         if (a->work_end > 0) we = a->work_end;
         if (wb < 0 || we > total || wb > we) return fail(GNA_EINVAL, "work range outside [0, n_work] or begin > end");
     }
-    if (we - wb >= (1LL << 31) - (1LL << 20)) return fail(GNA_EINVAL, "work range longer than 2^31 - 2^20 items: split the launch");
     p.work_begin = wb;
     p.work_end = we;
     p.o_perm = c.ws ? c.ws + c.L.o : nullptr;

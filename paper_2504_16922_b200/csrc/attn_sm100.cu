@@ -115,10 +115,8 @@ __global__ void __launch_bounds__(384, 1)
     }
 
     // ---------------------------------------------------------- this CTA's items
-    // 32-bit item counters (the host limits a launch's range to < 2^31 - 2^20 items): fewer live
-    // registers in the 64-register control warps and across the softmax stage loop
-    const int n_range = static_cast<int>(p.work_end - p.work_begin);
-    const int first = blockIdx.x, step = gridDim.x;
+    const long long n_range = p.work_end - p.work_begin;
+    const long long first = blockIdx.x, step = gridDim.x;
     // global work index w -> (unit bh, item index widx)
     auto decode_w = [&](long long w, long long& bh, long long& widx) {
         if ((w | p.n_items) < (1LL << 31)) {
@@ -279,7 +277,7 @@ __global__ void __launch_bounds__(384, 1)
                 };
                 if (warp == 10) {
                     int kq = 0;
-                    for (int t = first; t < n_range; t += step, ++kq) {
+                    for (long long t = first; t < n_range; t += step, ++kq) {
                         long long bh, widx;
                         decode_w(p.work_begin + t, bh, widx);
                         const int4 item = __ldg(p.items + widx);
@@ -340,7 +338,7 @@ __global__ void __launch_bounds__(384, 1)
                     uint32_t ph = 0;
                     bool first_load = true;
                     StageBoxes sb;
-                    for (int t = first; t < n_range; t += step) {
+                    for (long long t = first; t < n_range; t += step) {
                         long long bh, widx;
                         decode_w(p.work_begin + t, bh, widx);
                         const int4 item = __ldg(p.items + widx);
@@ -395,7 +393,7 @@ __global__ void __launch_bounds__(384, 1)
             // the staging buffer to be read and hands it back
             if (p.tma_store) {
                 int nu[2] = {0, 0};
-                for (int t = first; t < n_range; t += step) {
+                for (long long t = first; t < n_range; t += step) {
                     long long bh, widx;
                     decode_w(p.work_begin + t, bh, widx);
                     const int4 item = __ldg(p.items + widx);
@@ -495,7 +493,7 @@ __global__ void __launch_bounds__(384, 1)
                 int pc[2] = {0, 0};   // stages consumed per sub-tile (P barrier phases)
                 int ni[2] = {0, 0};   // items seen per sub-tile (O barrier phases)
                 int kq = 0;
-                for (int t = first; t < n_range; t += step, ++kq) {
+                for (long long t = first; t < n_range; t += step, ++kq) {
                     long long bh, widx;
                     decode_w(p.work_begin + t, bh, widx);
                     const int4 item = __ldg(p.items + widx);
@@ -586,7 +584,7 @@ __global__ void __launch_bounds__(384, 1)
         int kq = 0;
         int nuse = 0;  // O staging buffer uses (both WGs) before the current item
         int nturn = 0;  // exp phases this WG ran in two-sub-tile items (GNA_EXP_MUTEX token phases)
-        for (int t = first; t < n_range; t += step, ++kq) {
+        for (long long t = first; t < n_range; t += step, ++kq) {
             long long bh, widx;
             decode_w(p.work_begin + t, bh, widx);
             const int4 item = __ldg(p.items + widx);
@@ -872,8 +870,8 @@ __global__ void __launch_bounds__(384, 1)
 
             // ---------------------------------------------------------- epilogue
             // the row's position, recomputed from the (laundered) work index
-            int t_e = t;
-            asm volatile("" : "+r"(t_e));
+            long long t_e = t;
+            asm volatile("" : "+l"(t_e));
             decode_w(p.work_begin + t_e, bh, widx);
             const int4 item_e = __ldg(p.items + widx);
             const int4 cc4 = __ldg(p.item_info + 3 * widx + 2);
