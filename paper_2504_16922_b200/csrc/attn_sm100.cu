@@ -22,9 +22,9 @@
 // FMHA the paper builds on; this is an independent sm_100a design).
 //
 // Softmax (online): S is read from TMEM; the fine-grained GNA mask
-// is applied only when some row of the warp does not cover every
-// key of the stage (per-warp generalisation of the paper's perfectly
-// block-sparse predicate, future work P:1054-1058).  The running
+// is applied only to the stage halves (boxes) that some row of the
+// warp does not fully cover (per-warp, per-box generalisation of the paper's
+// perfectly block-sparse predicate, future work P:1054-1058).  The running
 // max used for exp2 is only raised when the row max grows by > 8 (log2
 // units), so O in TMEM is rescaled rarely (threshold trick; values of P stay
 // <= 2^8, exact in bf16 range).
@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(384, 1)
     constexpr bool F16 = DT == 1;
     using C = Cfg<DP, BV, F8>;
     constexpr int KPB = C::KPB;
-    static_assert(!F8 || (DP == 128 && GNA_PSPLIT <= 2), "E4M3 path: head_dim 128, P split 1 or 2");
+    // P chunks handed to the MMA per stage (the E4M3 path supports 1 or 2)
+    constexpr int PS = (F8 && GNA_PSPLIT > 2) ? 2 : GNA_PSPLIT;
+    static_assert(!F8 || DP == 128, "E4M3 path: head_dim 128");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* sgen = smem_raw + (sbase - ptx::smem_u32(smem_raw));
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(384, 1)
                         // GNA_B_DELAY: start sub-tile B's pipeline later (after A's first P chunk / full P
                         // of stage 0) so the two softmax warpgroups' exp phases, which share the SMSPs'
                         // MUFU units, overlap less (the steady-state A/B offset keeps the initial one)
-                        if (GNA_B_DELAY == 1 && GNA_PSPLIT > 1) ptx::mbar_wait(bar_pc0, pc[0] & 1);
+                        if (GNA_B_DELAY == 1 && PS > 1) ptx::mbar_wait(bar_pc0, pc[0] & 1);
                         if (GNA_B_DELAY == 2) ptx::mbar_wait(bar_p_full0, pc[0] & 1);
                         issue_qk(1, q16b, slotK * TILE16);
                         GNA_COMMIT(bar_s_full0 + 8);
@@ -531,16 +533,16 @@ __global__ void __launch_bounds__(384, 1)
                             // have drained it from TMEM
                             if (j == 0 && ni[i] > 0) ptx::mbar_wait(bar_o_free0 + 8 * i, (ni[i] - 1) & 1);
 #pragma unroll
-                            for (int c = 0; c < GNA_PSPLIT - 1; ++c) {
+                            for (int c = 0; c < PS - 1; ++c) {
                                 ptx::mbar_wait(bar_pc0 + 8 * (3 * i + c), pc[i] & 1);
                                 ptx::tc_fence_after();
-                                issue_pv(i, slotV * TILE16, j > 0 || c > 0, c * KP / GNA_PSPLIT,
-                                         (c + 1) * KP / GNA_PSPLIT);
+                                issue_pv(i, slotV * TILE16, j > 0 || c > 0, c * KP / PS,
+                                         (c + 1) * KP / PS);
                             }
                             ptx::mbar_wait(bar_p_full0 + 8 * i, pc[i] & 1);
                             if (lane == 0) GT(j, 9 + i);
                             ptx::tc_fence_after();
-                            issue_pv(i, slotV * TILE16, j > 0 || GNA_PSPLIT > 1, (GNA_PSPLIT - 1) * KP / GNA_PSPLIT, KP);
+                            issue_pv(i, slotV * TILE16, j > 0 || PS > 1, (PS - 1) * KP / PS, KP);
                             ++pc[i];
                             if (!has_next) GNA_COMMIT(bar_o_full0 + 8 * i);  // O_i final for this item
                             if (i == 0 && has_next) {
@@ -751,7 +753,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     m_tile = ptx::max3(mx0, mx1, fmaxf(mx2, mx3)) * sl2;
                 }
-                constexpr int CH = 64 / GNA_PSPLIT;  // key pairs per P chunk
+                constexpr int CH = 64 / PS;  // key pairs per P chunk
                 float la0 = 0.f, la1 = 0.f, lb0 = 0.f, lb1 = 0.f;
                 uint32_t pk[64];
                 // 2^x of key pair pi: x = s * scale*log2(e) - m (FFMA2), 2^x on MUFU or, for 1 pair in
